@@ -1,0 +1,141 @@
+/*
+ * venom.h — C ABI of libvenom: the B200 (sm_100a) hot path of VENOM / Spatha (arXiv 2310.02065).
+ *
+ * The three calls are the operations the paper defines:
+ *   venom_compress   dense weight -> V:N:M (values, metadata, column_idx)   PAPER.md:187-195 (§3)
+ *   venom_spmm       C = A_vnm · B (+ bias) on the compressed operand       PAPER.md:197-263 (§4),
+ *                    bias as in spatha.spmm(values, columns, metadata, input, bias)
+ *   venom_decompress V:N:M -> dense (inverse of Fig 3; verification / dense-baseline operand)
+ *
+ * Notation: C[R×T] = A[R×K] · B[K×T]. A is cut into V-row × M-column blocks;
+ * each block keeps 4 columns (column_idx) and each row keeps 2 of those 4 (values + 2-bit
+ * m-indices packed as metadata nibbles). N is fixed at 2 (fp16/bf16 sparse tensor cores are 2:4,
+ * PAPER.md:144). G = K/M groups per row.
+ *
+ * Canonical byte layouts (what "bit-exact" is checked on; readings #7-#10):
+ *   values     dtype[R][G][2]            the two kept weights of (row, group), original bits,
+ *                                        ordered by ascending m-index. Row-major R × (2G).
+ *   metadata   uint8[R][ceil(G/2)]       nibble(r,g) = p0 | p1<<2 with p0 < p1 in [0,4) the
+ *                                        m-indices; byte h of row r = nib(r,2h) | nib(r,2h+1)<<4;
+ *                                        an odd G leaves the last high nibble 0.
+ *   column_idx uint8[R/V][G][4]          the block's 4 selected columns, block-relative in [0,M),
+ *                                        strictly ascending.
+ *
+ * Conventions
+ *   - Every data pointer is a DEVICE pointer owned by the caller. The library never allocates,
+ *     never synchronises `stream`, and keeps no mutable global state (thread-safe; the only
+ *     process-wide state is the lazily resolved driver entry point cuTensorMapEncodeTiled).
+ *   - Argument, shape and architecture errors are returned synchronously and nothing is launched.
+ *   - Data-dependent errors (non-finite input, corrupt metadata) are reported on the device by
+ *     atomicMax()-ing a venom_status_t into *dev_status (nullable: NULL skips those checks); the
+ *     outputs are undefined when that word becomes non-zero. The caller zeroes it.
+ *   - Buffers must stay valid until the stream work completes.
+ */
+#ifndef VENOM_H_
+#define VENOM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VENOM_OK = 0,
+  VENOM_ERR_INVALID_ARGUMENT = 1,    /* null pointer, ld < cols, misalignment, bad sizes          */
+  VENOM_ERR_NON_DIVISIBLE_ROWS = 2,  /* V does not divide R              */
+  VENOM_ERR_NON_DIVISIBLE_COLS = 3,  /* M does not divide K              */
+  VENOM_ERR_UNSUPPORTED_PATTERN = 4, /* N != 2, M < 4, M > 256; spmm: V not in {32,64} ∪ 128ℕ,
+                                        G % 4 != 0                                               */
+  VENOM_ERR_UNSUPPORTED_DTYPE = 5,
+  VENOM_ERR_NON_FINITE = 6,          /* device-reported (finite inputs only)         */
+  VENOM_ERR_CORRUPT_METADATA = 7,    /* device-reported: m-indices not ascending, column_idx not
+                                        strictly ascending or >= M                  */
+  VENOM_ERR_ARCH = 8,                /* current device is not sm_100                             */
+  VENOM_ERR_CUDA = 9                 /* launch / driver error                                    */
+} venom_status_t;
+
+typedef enum { VENOM_F16 = 0, VENOM_BF16 = 1 } venom_dtype_t;
+
+/* V:N:M pattern. n must be 2. */
+typedef struct {
+  int32_t v, n, m;
+} venom_format_t;
+
+/* Opaque CUDA stream (cudaStream_t); 0 = legacy default stream. */
+typedef void* venom_stream_t;
+
+/* Sizes of the three compressed arrays for an R×K matrix (PAPER.md:194-195:
+ * values R×K/M×2, column-loc R/V×K/M×4). Host-only, no device access. */
+venom_status_t venom_compressed_sizes(int64_t R, int64_t K, venom_format_t f,
+                                      int64_t* values_elems,      /* R*(K/M)*2        */
+                                      int64_t* metadata_bytes,    /* R*ceil((K/M)/2)  */
+                                      int64_t* column_idx_bytes); /* (R/V)*(K/M)*4    */
+
+/*
+ * Magnitude V:N:M compression: per V×M block, the 4 columns with the largest
+ * L1 mass over the block's V rows (fp64, ascending rows; ties -> lower index), then per row the 2
+ * largest |w| among those 4 (ties -> lower m-index). Bit-identical to the CPU oracle.
+ *   A          dtype[R][lda], row-major, lda >= K
+ *   values, metadata, column_idx   outputs in the canonical layouts above
+ * Requirements: any V >= 1 with V | R, 4 <= M <= 256 with M | K, n == 2. No alignment demands.
+ */
+venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda,
+                              venom_dtype_t dt, venom_format_t f,
+                              void* values, uint8_t* metadata, uint8_t* column_idx,
+                              int32_t* dev_status, venom_stream_t stream);
+
+/*
+ * Inverse of the format: A_out[i][g*M + column_idx[i/V][g][p]] = value with
+ * m-index p; every other element is +0.0. A_out is dtype[R][lda], lda >= K.
+ */
+venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
+                                const uint8_t* column_idx, int64_t R, int64_t K,
+                                venom_dtype_t dt, venom_format_t f,
+                                void* A_out, int64_t lda,
+                                int32_t* dev_status, venom_stream_t stream);
+
+/*
+ * SpMM  C = decompress(A) · B (+ bias), fp32 accumulation, round-to-nearest-even to dtype
+ * (PAPER.md:207-209 mapping onto 2:4 sparse tensor cores; reading #13).
+ *   B     dtype[K][ldb] row-major (T contiguous; for a Linear layer, the feature-major activation)
+ *   C     dtype[R][ldc] row-major
+ *   bias  nullable dtype[R], added in fp32 before rounding
+ * Requirements (else VENOM_ERR_UNSUPPORTED_PATTERN / INVALID_ARGUMENT):
+ *   V in {32, 64} or V % 128 == 0, V | R; M in [4,256], M | K; G = K/M with G % 4 == 0;
+ *   T % 8 == 0, ldb % 8 == 0, ldc % 8 == 0, ldb >= T, ldc >= T; values/B/C 16-byte aligned.
+ * Metadata validity is NOT checked here (use venom_decompress with dev_status to validate);
+ * malformed metadata gives undefined values, never out-of-bounds accesses.
+ */
+venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
+                          int64_t R, int64_t K, venom_format_t f,
+                          const void* B, int64_t T, int64_t ldb,
+                          void* C, int64_t ldc,
+                          const void* bias,
+                          venom_dtype_t dt, venom_stream_t stream);
+
+/* Optional tile override for venom_spmm (benchmarking / tuning). Zero fields = library default.
+ * tile_t: output columns per CTA tile (64, 128 or 256); stages: pipeline depth. */
+typedef struct {
+  int32_t tile_t;
+  int32_t stages;
+  int32_t max_ctas;  /* persistent grid cap (0 = #SMs) */
+} venom_spmm_opts_t;
+
+venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
+                             int64_t R, int64_t K, venom_format_t f,
+                             const void* B, int64_t T, int64_t ldb,
+                             void* C, int64_t ldc, const void* bias,
+                             venom_dtype_t dt, const venom_spmm_opts_t* opts,
+                             venom_stream_t stream);
+
+/* Number of kernels venom_spmm / venom_compress / venom_decompress launch per call (1 each). */
+int32_t venom_kernels_per_call(void);
+
+const char* venom_status_string(venom_status_t s);
+const char* venom_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VENOM_H_ */

@@ -1,0 +1,202 @@
+"""venom-b200: the data-parallel hot path of VENOM / Spatha (arXiv 2310.02065) for NVIDIA B200.
+
+Thin ctypes binding over ``libvenom.so`` (C ABI in ``include/venom.h``). This module only
+marshals arguments: PyTorch provides device memory and the current stream; every step of the
+path (compression, decompression, SpMM) runs in the sm_100a kernels of ``csrc/``. There is no
+CPU fallback: if the library is missing or the device is not sm_100, calls raise.
+
+Paper vocabulary: a V:N:M matrix keeps, per V×M block, 4 columns
+(``column_idx``, the paper's *column-loc*) and per row 2 of those 4 (``values`` + 2-bit
+*m-indices* packed in ``metadata``). ``spmm`` computes C = A·B (+ bias) like
+``spatha.spmm(values, columns, metadata, input, bias)``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvenom.so")
+
+OK = 0
+STATUS_NAMES = {
+    0: "VENOM_OK", 1: "VENOM_ERR_INVALID_ARGUMENT", 2: "VENOM_ERR_NON_DIVISIBLE_ROWS",
+    3: "VENOM_ERR_NON_DIVISIBLE_COLS", 4: "VENOM_ERR_UNSUPPORTED_PATTERN",
+    5: "VENOM_ERR_UNSUPPORTED_DTYPE", 6: "VENOM_ERR_NON_FINITE", 7: "VENOM_ERR_CORRUPT_METADATA",
+    8: "VENOM_ERR_ARCH", 9: "VENOM_ERR_CUDA",
+}
+EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
+            "venom_spmm_ex", "venom_kernels_per_call", "venom_status_string", "venom_version"]
+
+
+class VenomError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {STATUS_NAMES.get(status, status)}")
+        self.status = status
+
+
+class _Format(ctypes.Structure):
+    _fields_ = [("v", ctypes.c_int32), ("n", ctypes.c_int32), ("m", ctypes.c_int32)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libvenom.so (built by ``build()`` / ``__graft_entry__.build()``); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libvenom.so not built ({LIB_PATH}); run python -m "
+                               "paper_2310_02065_b200.build — there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        L.venom_compressed_sizes.argtypes = [I64, I64, _Format, P, P, P]
+        L.venom_compress.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P]
+        L.venom_decompress.argtypes = [P, P, P, I64, I64, ctypes.c_int, _Format, P, I64, P, P]
+        L.venom_spmm.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int, P]
+        L.venom_spmm_ex.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int,
+                                    ctypes.POINTER(_Opts), P]
+        for fn in ("venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
+                   "venom_spmm_ex"):
+            getattr(L, fn).restype = ctypes.c_int
+        L.venom_status_string.argtypes = [ctypes.c_int]
+        L.venom_status_string.restype = ctypes.c_char_p
+        L.venom_version.restype = ctypes.c_char_p
+        L.venom_kernels_per_call.restype = I32
+        _lib = L
+    return _lib
+
+
+def build(force: bool = False) -> str:
+    from .build import build as _b
+    return _b(force=force)
+
+
+def _dt(t: torch.dtype) -> int:
+    if t == torch.float16:
+        return 0
+    if t == torch.bfloat16:
+        return 1
+    raise VenomError(5, f"dtype {t}")
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise VenomError(st, what)
+
+
+@dataclass
+class VNMTensor:
+    """A V:N:M-compressed R×K matrix (Fig 3). N is always 2."""
+    values: torch.Tensor      # dtype[R, K/M, 2]
+    metadata: torch.Tensor    # uint8[R, ceil(K/M/2)]
+    column_idx: torch.Tensor  # uint8[R/V, K/M, 4]
+    R: int
+    K: int
+    V: int
+    M: int
+    N: int = 2
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.values.dtype
+
+    @property
+    def nnz(self) -> int:
+        return self.R * (self.K // self.M) * 2
+
+    def fmt(self) -> _Format:
+        return _Format(self.V, self.N, self.M)
+
+
+def compressed_sizes(R: int, K: int, V: int, M: int, N: int = 2):
+    nv, nm, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().venom_compressed_sizes(R, K, _Format(V, N, M), ctypes.byref(nv), ctypes.byref(nm),
+                                        ctypes.byref(nc)), "venom_compressed_sizes")
+    return nv.value, nm.value, nc.value
+
+
+def compress(A: torch.Tensor, V: int, M: int, N: int = 2, status: Optional[torch.Tensor] = None,
+             check: bool = False) -> VNMTensor:
+    """Magnitude V:N:M compression on the GPU. ``status`` (int32[1] on the
+    device) receives data-dependent errors; ``check=True`` allocates one and synchronises to read
+    it (raising on non-finite input)."""
+    assert A.is_cuda and A.dim() == 2 and A.stride(1) == 1, "A: 2-D CUDA tensor, unit column stride"
+    R, K = A.shape
+    nv, nm, nc = compressed_sizes(R, K, V, M, N)
+    G = K // M
+    values = torch.empty((R, G, 2), dtype=A.dtype, device=A.device)
+    metadata = torch.empty((R, (G + 1) // 2), dtype=torch.uint8, device=A.device)
+    column_idx = torch.empty((R // V, G, 4), dtype=torch.uint8, device=A.device)
+    if check and status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=A.device)
+    st = lib().venom_compress(ctypes.c_void_p(A.data_ptr()), R, K, A.stride(0), _dt(A.dtype),
+                              _Format(V, N, M), ctypes.c_void_p(values.data_ptr()),
+                              ctypes.c_void_p(metadata.data_ptr()), ctypes.c_void_p(column_idx.data_ptr()),
+                              ctypes.c_void_p(status.data_ptr() if status is not None else 0),
+                              _stream(A.device))
+    _check(st, "venom_compress")
+    if check:
+        s = int(status.item())
+        _check(s, "venom_compress (device status)")
+    return VNMTensor(values, metadata, column_idx, R, K, V, M, N)
+
+
+def decompress(x: VNMTensor, out: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None,
+               check: bool = False) -> torch.Tensor:
+    """V:N:M -> dense (inverse of Fig 3); +0.0 at every pruned position."""
+    if out is None:
+        out = torch.empty((x.R, x.K), dtype=x.dtype, device=x.values.device)
+    assert out.stride(1) == 1
+    if check and status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=out.device)
+    st = lib().venom_decompress(ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
+                                ctypes.c_void_p(x.column_idx.data_ptr()), x.R, x.K, _dt(x.dtype), x.fmt(),
+                                ctypes.c_void_p(out.data_ptr()), out.stride(0),
+                                ctypes.c_void_p(status.data_ptr() if status is not None else 0),
+                                _stream(out.device))
+    _check(st, "venom_decompress")
+    if check:
+        _check(int(status.item()), "venom_decompress (device status)")
+    return out
+
+
+def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
+         out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
+         max_ctas: int = 0) -> torch.Tensor:
+    """C = A_vnm · B (+ bias) on the sparse tensor cores.
+    B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T]."""
+    assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[0] == x.K
+    assert B.dtype == x.dtype
+    T = B.shape[1]
+    if out is None:
+        out = torch.empty((x.R, T), dtype=x.dtype, device=B.device)
+    assert out.stride(1) == 1 and out.shape == (x.R, T)
+    if bias is not None:
+        assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
+    opts = _Opts(tile_t, stages, max_ctas)
+    st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
+                             ctypes.c_void_p(x.column_idx.data_ptr()), x.R, x.K, x.fmt(),
+                             ctypes.c_void_p(B.data_ptr()), T, B.stride(0),
+                             ctypes.c_void_p(out.data_ptr()), out.stride(0),
+                             ctypes.c_void_p(bias.data_ptr() if bias is not None else 0),
+                             _dt(x.dtype), ctypes.byref(opts), _stream(B.device))
+    _check(st, "venom_spmm")
+    return out
+
+
+def version() -> str:
+    return lib().venom_version().decode()

@@ -1,0 +1,372 @@
+// spmm_kernel.cuh — V:N:M SpMM  C = A_vnm · B (+ bias)  for sm_100a.
+//
+// The paper's Spatha kernel (§4.1) is an Ampere design: cp.async staging,
+// mma.sp m16n8k32 from registers, padded SMEM epilogue. What carries over to Blackwell is the
+// mapping (Fig 4): per V-block, gather only the 4 selected rows of B for every
+// group of M columns (through column-loc), so the block becomes a plain 2:4 sparse product over
+// the condensed dimension K' = 4·K/M that the sparse tensor cores execute natively.
+//
+// B200 design:
+//   * persistent CTAs (one per SM), static round-robin tile schedule, tiles of 128 rows × BN cols;
+//   * warp 0  producer: column_idx words -> 4 B-row coordinates per group, TMA tile::gather4 of
+//             the selected rows (the paper's stage 1₂ "only the rows of B selected by column-loc")
+//             plus a TMA tile load of the compressed values; column_idx is register-prefetched
+//             several stages ahead (the paper's stage 1₁ "two-level pre-fetching");
+//   * warps 6-9 metadata: canonical per-row nibbles -> the tensor-core metadata layout in SMEM
+//             ("we also load directly ... the m-indices"), prefetched ahead;
+//   * warp 1  MMA: tcgen05.cp metadata SMEM->TMEM, tcgen05.mma.sp (M=128, N=BN, K=32) with fp32
+//             accumulation in TMEM (the paper's stage 2 on 5th-gen sparse tensor cores);
+//   * warps 2-5 epilogue: tcgen05.ld -> +bias -> round -> 16-byte global stores (stage 3),
+//             overlapped with the next tile's main loop when TMEM allows two accumulators.
+// V = 128·k uses one V-block per tile; V ∈ {32, 64} packs NB = 128/V blocks into one 128-row A
+// tile and issues one MMA per block (each block has its own gathered B' and accumulator).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "ptx_sm100.cuh"
+
+namespace venom {
+
+struct SpmmParams {
+  const uint8_t* metadata;
+  const uint8_t* column_idx;
+  const uint16_t* bias;
+  uint16_t* C;
+  int64_t R, K, T, ldc;
+  int V, M, G, meta_row;
+  int num_ks;    // k-stages per tile = ceil(G / 32)
+  int m_tiles;   // ceil(R / 128)
+  int n_tiles;   // ceil(T / BN)
+  int num_tiles;
+  int is_bf16;
+};
+
+template <int NB_, int BN_, int STAGES_>
+struct SpmmCfg {
+  static constexpr int NB = NB_;              // V-blocks per 128-row tile
+  static constexpr int BN = BN_;              // output columns per tile (MMA N)
+  static constexpr int STAGES = STAGES_;
+  static constexpr int BM = 128;              // MMA M
+  static constexpr int KG = 32;               // groups per k-stage: K' = 128, 4 MMAs of K = 32
+  static constexpr int A_BYTES = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
+  static constexpr int B_CHUNK = 128 * 128;   // 128 K'-rows × 64 columns × 2 B (SW128, MN-major)
+  static constexpr int B_BYTES = (BN / 64) * B_CHUNK;
+  static constexpr int E_BYTES = 128 * 16;    // 128 lanes × 4 metadata words
+  static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES + E_BYTES;
+  static constexpr int TX_BYTES = A_BYTES + NB * B_BYTES;
+  static constexpr int ACC_COLS = NB * BN;
+  static constexpr int E_COLS = 8;            // two 4-column metadata regions
+  static constexpr int ACC_BUFS = (2 * ACC_COLS + E_COLS <= 512) ? 2 : 1;
+  static constexpr int E_COL = 512 - E_COLS;
+  static constexpr int NUM_THREADS = 320;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
+  static_assert(ACC_BUFS * ACC_COLS + E_COLS <= 512, "TMEM budget");
+  static_assert(STAGE_BYTES % 1024 == 0, "stage alignment");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+};
+
+constexpr int kPrefetch = 4;  // register prefetch depth of column_idx / metadata (k-stages)
+
+template <bool kBF16>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (kBF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+// Canonical metadata of one row for one k-stage (32 groups = 16 bytes): the four 32-bit words
+// (one per K=32 MMA; group 8·kb+q in bits 4q..4q+3). Groups past G and rows past R read as the
+// valid all-zero-value pattern 0x4 (m-indices 0,1).
+__device__ __forceinline__ void load_meta_stage(const SpmmParams& p, int64_t row, int ks,
+                                                uint32_t (&w)[4]) {
+  if (row >= p.R) {
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) w[kb] = 0x44444444u;
+    return;
+  }
+  const uint8_t* base = p.metadata + row * p.meta_row + ks * 16;
+  const int g_left = p.G - ks * 32;  // groups of this stage that exist (multiple of 4)
+  if (g_left >= 32 && (p.meta_row & 15) == 0) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(base));
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    return;
+  }
+  // halfword granularity (meta_row is even because G % 4 == 0); tail halfwords -> 0x4444
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    uint32_t lo = 0x4444u, hi = 0x4444u;
+    if (8 * kb + 4 <= g_left) lo = __ldg(reinterpret_cast<const uint16_t*>(base) + 2 * kb);
+    if (8 * kb + 8 <= g_left) hi = __ldg(reinterpret_cast<const uint16_t*>(base) + 2 * kb + 1);
+    w[kb] = lo | (hi << 16);
+  }
+}
+
+template <class Cfg, bool kBF16>
+__global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
+    vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
+                    const __grid_constant__ CUtensorMap tm_b, const SpmmParams p) {
+  using namespace ptx;
+  constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
+
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  // bars: full[STAGES], empty[STAGES], acc_full[2], acc_empty[2]; then the TMEM base word
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = full0 + 8 * STAGES;
+  const uint32_t accf0 = empty0 + 8 * STAGES;
+  const uint32_t acce0 = accf0 + 16;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const uint32_t smem0 = smem_u32(smem);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1 + 4);  // producer expect_tx + 4 metadata warps
+      mbar_init(empty0 + 8 * s, 1);     // MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);      // MMA commit
+      mbar_init(acce0 + 8 * b, 4);      // 4 epilogue warps
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_values);
+    prefetch_tmap(&tm_b);
+  }
+  if (warp == 1) tmem_alloc<512>(smem_u32(tmem_base_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  const int my_tiles =
+      (static_cast<int>(blockIdx.x) < p.num_tiles)
+          ? (p.num_tiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                static_cast<int>(gridDim.x)
+          : 0;
+  const int total = my_tiles * p.num_ks;  // k-stage iterations this CTA runs
+  const int nrb = static_cast<int>(p.R / p.V);
+
+  auto tile_of = [&](int tl, int& m_tile, int& n_tile) {
+    const int t = static_cast<int>(blockIdx.x) + tl * static_cast<int>(gridDim.x);
+    n_tile = t / p.m_tiles;  // T-band order: all row tiles of one column band first
+    m_tile = t - n_tile * p.m_tiles;
+  };
+  auto block_of = [&](int m_tile, int b) -> int {
+    const int rb = (NB == 1) ? (m_tile * 128) / p.V : m_tile * NB + b;
+    return rb < nrb ? rb : nrb - 1;  // padding block of a ragged last tile: any valid block
+  };
+
+  if (warp == 0) {
+    // ======================= producer: values tile + gathered B' rows =======================
+    const uint64_t pol_a = policy_evict_first();
+    const uint64_t pol_b = policy_evict_last();
+    uint32_t cw[kPrefetch][NB];
+    auto fetch = [&](int it, uint32_t (&w)[NB]) {
+      if (it >= total) return;
+      int m_tile, n_tile;
+      tile_of(it / p.num_ks, m_tile, n_tile);
+      const int gg = (it % p.num_ks) * Cfg::KG + lane;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        w[b] = (gg < p.G) ? __ldg(reinterpret_cast<const uint32_t*>(p.column_idx) +
+                                  static_cast<int64_t>(block_of(m_tile, b)) * p.G + gg)
+                          : 0u;
+    };
+#pragma unroll
+    for (int j = 0; j < kPrefetch; ++j) fetch(j, cw[j]);
+    for (int it0 = 0; it0 < total; it0 += kPrefetch) {
+#pragma unroll
+      for (int j = 0; j < kPrefetch; ++j) {
+        const int it = it0 + j;
+        if (it < total) {
+          const int stage = it % STAGES;
+          const uint32_t phase = (it / STAGES) & 1;
+          int m_tile, n_tile;
+          tile_of(it / p.num_ks, m_tile, n_tile);
+          const int ks = it % p.num_ks;
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
+          if (lane == 0) {
+            mbar_arrive_expect_tx(full0 + 8 * stage, Cfg::TX_BYTES);
+            tma_load_2d(sbase, &tm_values, full0 + 8 * stage, ks * 64, m_tile * 128, pol_a);
+          }
+          __syncwarp();
+          const int gg = ks * Cfg::KG + lane;
+          const int col0 = n_tile * BN;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            int r[4];
+            const uint32_t w = cw[j][b];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              r[t] = (gg < p.G) ? gg * p.M + static_cast<int>((w >> (8 * t)) & 0xFF)
+                                : static_cast<int>(p.K);  // past the last row: zero fill
+            const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + lane * 512;
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_gather4(bdst + c * Cfg::B_CHUNK, &tm_b, full0 + 8 * stage, col0 + 64 * c, r[0],
+                          r[1], r[2], r[3], pol_b);
+          }
+          fetch(it + kPrefetch, cw[j]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (one elected lane) =======================
+    constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128, BN);
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      const int ab = tl % Cfg::ACC_BUFS;
+      const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
+      mbar_wait(acce0 + 8 * ab, aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tile = tmem_base + ab * Cfg::ACC_COLS;
+      for (int ks = 0; ks < p.num_ks; ++ks) {
+        const int it = tl * p.num_ks + ks;
+        const int stage = it % STAGES;
+        mbar_wait(full0 + 8 * stage, (it / STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
+          const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * (it & 1);
+          // metadata: 128 rows × 16 B, core matrices of 8 rows contiguous (SBO = 128 B)
+          tc_cp_128x128b(e_tmem, smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0));
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            const uint32_t e_addr = e_tmem + kb;
+            const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
+            // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
+            const uint64_t adesc = smem_desc(sbase + kb * 32, 16, 1024, 2);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
+              // K advance 32 rows = 4096 B per MMA
+              const uint64_t bdesc =
+                  smem_desc(sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + kb * 4096, Cfg::B_CHUNK, 1024, 2);
+              tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
+                            (ks | kb) != 0 ? 1u : 0u);
+            }
+          }
+          tc_commit(empty0 + 8 * stage);
+          if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 2 && warp <= 5) {
+    // ======================= epilogue: TMEM -> +bias -> round -> global =======================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r_local = 32 * q + lane;
+    for (int tl = 0; tl < my_tiles; ++tl) {
+      int m_tile, n_tile;
+      tile_of(tl, m_tile, n_tile);
+      const int ab = tl % Cfg::ACC_BUFS;
+      mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(m_tile) * 128 + r_local;
+      const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
+      const float bv = (p.bias != nullptr && row < p.R)
+                           ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
+                                    : __half2float(__ushort_as_half(p.bias[row])))
+                           : 0.0f;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
+                             ab * Cfg::ACC_COLS + b * BN;
+      const int64_t col_base = static_cast<int64_t>(n_tile) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + 32 * c, v);
+        tmem_ld_wait();
+        const int64_t col = col_base + 32 * c;
+        if (row < p.R) {
+          uint16_t* dst = p.C + row * p.ldc + col;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (col + 8 * u < p.T) {
+              uint4 o;
+              o.x = pack2<kBF16>(__uint_as_float(v[8 * u + 0]) + bv, __uint_as_float(v[8 * u + 1]) + bv);
+              o.y = pack2<kBF16>(__uint_as_float(v[8 * u + 2]) + bv, __uint_as_float(v[8 * u + 3]) + bv);
+              o.z = pack2<kBF16>(__uint_as_float(v[8 * u + 4]) + bv, __uint_as_float(v[8 * u + 5]) + bv);
+              o.w = pack2<kBF16>(__uint_as_float(v[8 * u + 6]) + bv, __uint_as_float(v[8 * u + 7]) + bv);
+              *reinterpret_cast<uint4*>(dst + 8 * u) = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce0 + 8 * ab);
+    }
+  } else {
+    // ======================= metadata: canonical nibbles -> tensor-core layout =======================
+    // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
+    // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3.
+    const int L = 32 * (warp - 6) + lane;
+    const int m_a = (L & 7) + 16 * (L >> 4);
+    const int k1 = (L >> 3) & 1;
+    uint32_t wa[kPrefetch][4], wb[kPrefetch][4];
+    auto fetch = [&](int it, uint32_t (&xa)[4], uint32_t (&xb)[4]) {
+      if (it >= total) return;
+      int m_tile, n_tile;
+      tile_of(it / p.num_ks, m_tile, n_tile);
+      const int ks = it % p.num_ks;
+      const int64_t ra = static_cast<int64_t>(m_tile) * 128 + m_a;
+      load_meta_stage(p, ra, ks, xa);
+      load_meta_stage(p, ra + 8, ks, xb);
+    };
+#pragma unroll
+    for (int j = 0; j < kPrefetch; ++j) fetch(j, wa[j], wb[j]);
+    for (int it0 = 0; it0 < total; it0 += kPrefetch) {
+#pragma unroll
+      for (int j = 0; j < kPrefetch; ++j) {
+        const int it = it0 + j;
+        if (it < total) {
+          const int stage = it % STAGES;
+          uint32_t o[4];
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb)
+            o[kb] = ((wa[j][kb] >> (16 * k1)) & 0xFFFFu) | (((wb[j][kb] >> (16 * k1)) & 0xFFFFu) << 16);
+          mbar_wait(empty0 + 8 * stage, ((it / STAGES) & 1) ^ 1);
+          uint8_t* e_smem = smem + stage * Cfg::STAGE_BYTES + Cfg::A_BYTES + NB * Cfg::B_BYTES;
+          *reinterpret_cast<uint4*>(e_smem + 16 * L) = make_uint4(o[0], o[1], o[2], o[3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full0 + 8 * stage);
+          fetch(it + kPrefetch, wa[j], wb[j]);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// C = bias (or 0) when K == 0 (no groups): nothing to multiply.
+template <bool kBF16>
+__global__ void vnm_fill_bias_kernel(uint16_t* C, int64_t R, int64_t T, int64_t ldc,
+                                     const uint16_t* bias) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= R * T) return;
+  const int64_t r = idx / T, t = idx - r * T;
+  C[r * ldc + t] = bias ? bias[r] : static_cast<uint16_t>(0);
+}
+
+}  // namespace venom

@@ -1,0 +1,295 @@
+// venom_api.cu — the C ABI of libvenom (include/venom.h): argument validation, TMA descriptor
+// encoding and kernel launch. All compute runs in the kernels of format_kernels.cuh and
+// spmm_kernel.cuh; this file only marshals.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "../../include/venom.h"
+#include "format_kernels.cuh"
+#include "spmm_kernel.cuh"
+
+namespace {
+
+using venom::SpmmCfg;
+using venom::SpmmParams;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+venom_status_t check_arch() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return VENOM_ERR_CUDA;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+    return VENOM_ERR_CUDA;
+  if (major != 10 || minor != 0) return VENOM_ERR_ARCH;  // built for sm_100a only
+  return VENOM_OK;
+}
+
+venom_status_t validate_format(int64_t R, int64_t K, venom_format_t f) {
+  if (R < 0 || K < 0 || f.v < 1) return VENOM_ERR_INVALID_ARGUMENT;
+  if (f.n != 2 || f.m < 4 || f.m > 256) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (R % f.v != 0) return VENOM_ERR_NON_DIVISIBLE_ROWS;
+  if (K % f.m != 0) return VENOM_ERR_NON_DIVISIBLE_COLS;
+  return VENOM_OK;
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+venom_status_t launch_status() {
+  return cudaGetLastError() == cudaSuccess ? VENOM_OK : VENOM_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ SpMM dispatch
+template <class Cfg, bool kBF16>
+venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams p, int max_ctas,
+                        cudaStream_t s) {
+  auto kern = venom::vnm_spmm_kernel<Cfg, kBF16>;
+  // >= 116 KB of shared memory guarantees one CTA per SM (each CTA allocates all 512 TMEM columns)
+  const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return VENOM_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid < 1) return VENOM_OK;
+  kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tv, tb, p);
+  return launch_status();
+}
+
+template <class Cfg>
+venom_status_t run_spmm_dt(bool bf16, const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams p,
+                           int max_ctas, cudaStream_t s) {
+  return bf16 ? run_spmm<Cfg, true>(tv, tb, p, max_ctas, s)
+              : run_spmm<Cfg, false>(tv, tb, p, max_ctas, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* venom_version(void) { return "venom-b200 0.1 (sm_100a)"; }
+
+int32_t venom_kernels_per_call(void) { return 1; }
+
+const char* venom_status_string(venom_status_t s) {
+  switch (s) {
+    case VENOM_OK: return "ok";
+    case VENOM_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case VENOM_ERR_NON_DIVISIBLE_ROWS: return "V does not divide R";
+    case VENOM_ERR_NON_DIVISIBLE_COLS: return "M does not divide K";
+    case VENOM_ERR_UNSUPPORTED_PATTERN: return "unsupported V:N:M pattern";
+    case VENOM_ERR_UNSUPPORTED_DTYPE: return "unsupported dtype";
+    case VENOM_ERR_NON_FINITE: return "non-finite input";
+    case VENOM_ERR_CORRUPT_METADATA: return "corrupt metadata";
+    case VENOM_ERR_ARCH: return "device is not sm_100";
+    case VENOM_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+venom_status_t venom_compressed_sizes(int64_t R, int64_t K, venom_format_t f, int64_t* values_elems,
+                                      int64_t* metadata_bytes, int64_t* column_idx_bytes) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  if (values_elems) *values_elems = R * G * 2;
+  if (metadata_bytes) *metadata_bytes = R * ((G + 1) / 2);
+  if (column_idx_bytes) *column_idx_bytes = (R / f.v) * G * 4;
+  return VENOM_OK;
+}
+
+venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, venom_dtype_t dt,
+                              venom_format_t f, void* values, uint8_t* metadata,
+                              uint8_t* column_idx, int32_t* dev_status, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (lda < K) return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!A || !values || !metadata || !column_idx) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(values, 8) || !aligned(column_idx, 4) || !aligned(A, 2)) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  int gpc = 512 / f.m;
+  gpc -= gpc & 1;
+  if (gpc < 2) gpc = 2;
+  if (gpc > G + (G & 1)) gpc = static_cast<int>(G + (G & 1));
+  const dim3 grid(static_cast<unsigned>((G + gpc - 1) / gpc), static_cast<unsigned>(R / f.v));
+  if (grid.y > 65535u) return VENOM_ERR_INVALID_ARGUMENT;
+  const size_t smem = sizeof(double) * static_cast<size_t>(gpc) * f.m + 4 * static_cast<size_t>(gpc);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dt == VENOM_BF16)
+    venom::vnm_compress_kernel<true><<<grid, 256, smem, s>>>(
+        static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values),
+        metadata, column_idx, dev_status);
+  else
+    venom::vnm_compress_kernel<false><<<grid, 256, smem, s>>>(
+        static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values),
+        metadata, column_idx, dev_status);
+  return launch_status();
+}
+
+venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
+                                const uint8_t* column_idx, int64_t R, int64_t K, venom_dtype_t dt,
+                                venom_format_t f, void* A_out, int64_t lda, int32_t* dev_status,
+                                venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (lda < K) return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!values || !metadata || !column_idx || !A_out) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(values, 4) || !aligned(column_idx, 4) || !aligned(A_out, 2)) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool vec = aligned(A_out, 16) && (lda % 8 == 0);
+  const int kv = vec ? 8 : 1;
+  const int64_t work = R * ((K + kv - 1) / kv);
+  const int64_t blocks = (work + 255) / 256;
+  if (blocks > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  if (vec)
+    venom::vnm_decompress_kernel<8><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        static_cast<const uint16_t*>(values), metadata, column_idx, R, K, f.v, f.m, G,
+        static_cast<uint16_t*>(A_out), lda, dev_status);
+  else
+    venom::vnm_decompress_kernel<1><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        static_cast<const uint16_t*>(values), metadata, column_idx, R, K, f.v, f.m, G,
+        static_cast<uint16_t*>(A_out), lda, dev_status);
+  return launch_status();
+}
+
+venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
+                             int64_t R, int64_t K, venom_format_t f, const void* B, int64_t T,
+                             int64_t ldb, void* C, int64_t ldc, const void* bias, venom_dtype_t dt,
+                             const venom_spmm_opts_t* opts, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  const int V = f.v;
+  if (!(V == 32 || V == 64 || V % 128 == 0)) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  const int64_t G = K / f.m;
+  if (G % 4 != 0) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (T < 0 || ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || T == 0) return VENOM_OK;
+  if (!C || (K > 0 && (!values || !metadata || !column_idx || !B))) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(C, 16) || (K > 0 && (!aligned(values, 16) || !aligned(B, 16) || !aligned(column_idx, 4))))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (K > 0x7FFFFFFF || T > 0x7FFFFFFF || R > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool bf16 = dt == VENOM_BF16;
+
+  if (K == 0) {
+    const int64_t n = R * T;
+    if (bf16)
+      venom::vnm_fill_bias_kernel<true><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          static_cast<uint16_t*>(C), R, T, ldc, static_cast<const uint16_t*>(bias));
+    else
+      venom::vnm_fill_bias_kernel<false><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          static_cast<uint16_t*>(C), R, T, ldc, static_cast<const uint16_t*>(bias));
+    return launch_status();
+  }
+
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return VENOM_ERR_CUDA;
+  const int NB = (V % 128 == 0) ? 1 : 128 / V;
+  int tile_t = opts && opts->tile_t ? opts->tile_t : (NB == 1 ? 128 : (NB == 2 ? 64 : 64));
+  int stages = opts && opts->stages ? opts->stages : 0;
+  const int max_ctas = opts ? opts->max_ctas : 0;
+
+  // values: 2-D [R rows][2G] 16-bit, box 64 × 128 rows, 128B swizzle (UMMA K-major SW128)
+  CUtensorMap tv, tb;
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * G), static_cast<cuuint64_t>(R)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(4 * G)};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(values), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  }
+  // B: 2-D [K rows][T] 16-bit, box 64 × 1 row (gather4 fetches 4 rows), 128B swizzle
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(K)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldb)};
+    cuuint32_t box[2] = {64, 1};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(B), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  }
+
+  SpmmParams p;
+  p.metadata = metadata;
+  p.column_idx = column_idx;
+  p.bias = static_cast<const uint16_t*>(bias);
+  p.C = static_cast<uint16_t*>(C);
+  p.R = R;
+  p.K = K;
+  p.T = T;
+  p.ldc = ldc;
+  p.V = V;
+  p.M = f.m;
+  p.G = static_cast<int>(G);
+  p.meta_row = static_cast<int>((G + 1) / 2);
+  p.num_ks = static_cast<int>((G + 31) / 32);
+  p.m_tiles = static_cast<int>((R + 127) / 128);
+  p.is_bf16 = bf16;
+
+  auto set_tiles = [&](int bn) {
+    p.n_tiles = static_cast<int>((T + bn - 1) / bn);
+    p.num_tiles = p.m_tiles * p.n_tiles;
+  };
+  set_tiles(tile_t);
+  if (NB == 1) {
+    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2>>(bf16, tv, tb, p, max_ctas, s);
+    if (tile_t == 192) return run_spmm_dt<SpmmCfg<1, 192, 3>>(bf16, tv, tb, p, max_ctas, s);
+    if (tile_t == 128) {
+      if (stages == 2) return run_spmm_dt<SpmmCfg<1, 128, 2>>(bf16, tv, tb, p, max_ctas, s);
+      return run_spmm_dt<SpmmCfg<1, 128, 4>>(bf16, tv, tb, p, max_ctas, s);
+    }
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<1, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
+  } else if (NB == 2) {
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<2, 128, 2>>(bf16, tv, tb, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<2, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
+  } else {
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<4, 64, 2>>(bf16, tv, tb, p, max_ctas, s);
+  }
+  return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
+}
+
+venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
+                          int64_t R, int64_t K, venom_format_t f, const void* B, int64_t T,
+                          int64_t ldb, void* C, int64_t ldc, const void* bias, venom_dtype_t dt,
+                          venom_stream_t stream) {
+  return venom_spmm_ex(values, metadata, column_idx, R, K, f, B, T, ldb, C, ldc, bias, dt, nullptr,
+                       stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+"""C-ABI boundary checks that need no GPU: the library builds/loads, exports every symbol the
+header declares, and rejects bad arguments synchronously (before any device access)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2310_02065_b200 as venom
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "venom.h")).read()
+    return sorted(set(re.findall(r"\b(venom_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    venom.build()
+    return venom.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared_symbols()
+    assert {"venom_compress", "venom_spmm", "venom_decompress"} <= set(names)
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(venom.EXPORTED) == set(names)
+
+
+def test_status_strings_and_version(L):
+    assert L.venom_status_string(0) == b"ok"
+    assert b"sm_100a" in L.venom_version()
+    assert L.venom_kernels_per_call() == 1
+
+
+@pytest.mark.parametrize("R,K,V,N,M,expect", [
+    (1024, 4096, 64, 2, 8, 0), (10, 16, 4, 2, 8, 2), (8, 8, 4, 2, 3, 4), (8, 12, 4, 2, 8, 3),
+    (8, 16, 4, 3, 8, 4), (8, 512, 4, 2, 512, 4), (8, 16, 0, 2, 8, 1),
+])
+def test_compressed_sizes_and_validation(L, R, K, V, N, M, expect):
+    nv, nm, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    st = L.venom_compressed_sizes(R, K, venom._Format(V, N, M), ctypes.byref(nv), ctypes.byref(nm),
+                                  ctypes.byref(nc))
+    assert st == expect
+    if st == 0:
+        G = K // M
+        assert (nv.value, nm.value, nc.value) == (R * G * 2, R * ((G + 1) // 2), (R // V) * G * 4)
+
+
+def _spmm(L, R=256, K=512, V=128, M=8, T=64, ldb=64, ldc=64, n=2, dt=0):
+    P = ctypes.c_void_p
+    fake = P(0x10000)  # never dereferenced: validation fails first
+    return L.venom_spmm(fake, fake, fake, R, K, venom._Format(V, n, M), fake, T, ldb, fake, ldc,
+                        P(0), dt, P(0))
+
+
+def test_spmm_argument_errors(L):
+    assert _spmm(L, R=384, V=96) == 4          # V not in {32,64} ∪ 128N
+    assert _spmm(L, K=8 * 6, M=8) == 4         # G = 6, not a multiple of 4
+    assert _spmm(L, T=60, ldb=64, ldc=64) == 1  # T % 8
+    assert _spmm(L, ldb=32) == 1               # ldb < T
+    assert _spmm(L, ldc=68) == 1               # ldc % 8
+    assert _spmm(L, R=200) == 2                # V does not divide R
+    assert _spmm(L, K=500) == 3                # M does not divide K
+    assert _spmm(L, n=1) == 4
+    assert _spmm(L, dt=3) == 5
+
+
+def test_compress_argument_errors(L):
+    P = ctypes.c_void_p
+    f = P(0x10000)
+    assert L.venom_compress(f, 10, 16, 16, 0, venom._Format(4, 2, 8), f, f, f, P(0), P(0)) == 2
+    assert L.venom_compress(f, 8, 16, 8, 0, venom._Format(4, 2, 8), f, f, f, P(0), P(0)) == 1  # lda < K
+    assert L.venom_compress(f, 8, 16, 16, 7, venom._Format(4, 2, 8), f, f, f, P(0), P(0)) == 5
+    assert L.venom_decompress(f, f, f, 8, 16, 0, venom._Format(4, 2, 3), f, 16, P(0), P(0)) == 4
+
+
+def test_no_cpu_fallback_without_device(L):
+    """On a GPU-less host a valid call must fail loudly (CUDA / arch error), never compute."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    P = ctypes.c_void_p
+    buf = (ctypes.c_uint8 * 4096)()
+    p = P(ctypes.addressof(buf) + (16 - ctypes.addressof(buf) % 16) % 16)
+    st = L.venom_spmm(p, p, p, 128, 128, venom._Format(64, 2, 8), p, 8, 8, p, 8, P(0), 0, P(0))
+    assert st in (8, 9)

@@ -1,0 +1,294 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle on identical seeded
+inputs. Compressor / decompressor: bit-exact. SpMM: ‖C_gpu − C_ref‖_F / ‖C_ref‖_F ≤ 2e-3
+(BASELINE.json north_star) plus an element-wise bound, and exact probes (identity / one-hot B)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2310_02065_b200 as venom
+import synth
+from tests.helpers import BF16, F16, bits_to_f64, f64_to_bits, load_golden, rel_fro
+
+pytestmark = pytest.mark.gpu
+
+TOL_FRO = 2e-3  # north_star
+
+
+def tdt(dt):
+    return torch.float16 if dt == F16 else torch.bfloat16
+
+
+def to_dev(bits: np.ndarray, dt: int) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(tdt(dt)).cuda()
+
+
+def to_bits(t: torch.Tensor) -> np.ndarray:
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def gpu_compress(A_bits, dt, V, M):
+    A = to_dev(A_bits, dt)
+    x = venom.compress(A, V=V, M=M, check=True)
+    torch.cuda.synchronize()
+    return x, (to_bits(x.values), x.metadata.cpu().numpy(), x.column_idx.cpu().numpy())
+
+
+def check_spmm(C_gpu: torch.Tensor, C_ref: np.ndarray, dt: int):
+    got = bits_to_f64(to_bits(C_gpu), dt)
+    assert np.isfinite(got).all()
+    assert rel_fro(got, C_ref) <= TOL_FRO, rel_fro(got, C_ref)
+    # element-wise: output rounding (half ulp) + fp32 accumulation, scale-aware for cancellation
+    ulp = 2.0 ** -10 if dt == F16 else 2.0 ** -7
+    scale = np.sqrt(np.mean(C_ref ** 2)) + 1e-30
+    err = np.abs(got - C_ref)
+    assert (err <= ulp * np.abs(C_ref) + 1e-3 * scale).all(), float((err / (np.abs(C_ref) + scale)).max())
+
+
+# ------------------------------------------------------------------ compressor: bit-exact
+CASES = [
+    # (R, K, V, M, kind, dt)
+    (128, 128, 64, 8, "gauss", F16),          # configs[0] shape
+    (1024, 4096, 64, 8, "gauss", F16),        # configs[1] BERT-large FFN2
+    (256, 1024, 128, 16, "gauss", BF16),
+    (96, 280, 3, 7, "int", F16),
+    (64, 200, 32, 10, "special", F16),
+    (64, 200, 32, 10, "special", BF16),
+    (40, 500, 1, 100, "gauss", F16),
+    (512, 512, 256, 4, "int", BF16),
+    (128, 640, 64, 40, "sparse", F16),
+    (130, 256, 13, 32, "gauss", F16),
+    (64, 1280, 64, 20, "int", F16),
+    (16, 768, 8, 256, "gauss", BF16),
+    (48, 90, 16, 5, "special", F16),
+]
+
+
+def make_input(R, K, kind, dt, seed, M=8):
+    if kind == "gauss":
+        return synth.gaussian((R, K), 0.02, dt, seed)
+    if kind == "int":
+        return synth.small_integers((R, K), dt, seed)
+    if kind == "special":
+        return synth.special_values((R, K), dt, seed)
+    return synth.sparse_columns((R, K), dt, seed, live_cols_per_block=2, M=M)
+
+
+@pytest.mark.parametrize("R,K,V,M,kind,dt", CASES)
+def test_compress_bit_exact(R, K, V, M, kind, dt):
+    A = make_input(R, K, kind, dt, 1000 + R + K + V + M, M)
+    exp = oracle.compress(A, dt, V=V, M=M)
+    _, got = gpu_compress(A, dt, V, M)
+    for name, g, e in zip(("values", "metadata", "column_idx"), got, exp):
+        assert np.array_equal(g.reshape(e.shape), e), name
+
+
+@pytest.mark.parametrize("name", ["P1_spec_worked_example.json", "P2_greedy_not_joint.json",
+                                  "P3_fp64_exact_column_sums.json", "P4_raw_bits_and_zero_ties.json"])
+def test_compress_golden_on_gpu(name):
+    g = load_golden(name)
+    dt = F16
+    A = np.array(g["A_bits"], np.uint16) if "A_bits" in g else f64_to_bits(np.array(g["A"], float), dt)
+    _, (vals, meta, cidx) = gpu_compress(A, dt, g["V"], g["M"])
+    assert cidx.tolist() == g["expected_column_idx"]
+    assert meta.tolist() == g["expected_metadata"]
+    ev = np.array(g["expected_values_bits"], np.uint16) if "expected_values_bits" in g else \
+        f64_to_bits(np.array(g["expected_values"], float), dt)
+    assert np.array_equal(vals.reshape(ev.shape), ev)
+
+
+def test_compress_lda_view():
+    big = synth.gaussian((128, 700), 1.0, F16, 3)
+    A = to_dev(big, F16)[:, :640]
+    x = venom.compress(A, V=64, M=10, check=True)
+    exp = oracle.compress(big[:, :640], F16, V=64, M=10)
+    assert np.array_equal(to_bits(x.values).reshape(exp[0].shape), exp[0])
+    assert np.array_equal(x.metadata.cpu().numpy(), exp[1])
+    assert np.array_equal(x.column_idx.cpu().numpy(), exp[2])
+
+
+def test_compress_non_finite_status():
+    A = synth.gaussian((64, 64), 1.0, F16, 5)
+    A[3, 17] = 0x7C00
+    with pytest.raises(venom.VenomError) as e:
+        gpu_compress(A, F16, 32, 8)
+    assert e.value.status == 6
+
+
+# ------------------------------------------------------------------ decompressor: bit-exact
+@pytest.mark.parametrize("R,K,V,M,kind,dt", CASES[:8])
+def test_decompress_bit_exact(R, K, V, M, kind, dt):
+    A = make_input(R, K, kind, dt, 7 + R + K, M)
+    vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+    exp = oracle.decompress(vals, meta, cidx, R, K, dt, V, M)
+    x = venom.VNMTensor(to_dev(vals, dt), torch.from_numpy(meta).cuda(), torch.from_numpy(cidx).cuda(),
+                        R, K, V, M)
+    got = to_bits(venom.decompress(x, check=True))
+    assert np.array_equal(got, exp)
+
+
+def test_decompress_corrupt_metadata_status():
+    R, K, V, M = 64, 64, 32, 8
+    A = synth.gaussian((R, K), 1.0, F16, 9)
+    vals, meta, cidx = oracle.compress(A, F16, V=V, M=M)
+    meta = meta.copy()
+    meta[5, 2] = 0x11  # p0 == p1
+    x = venom.VNMTensor(to_dev(vals, F16), torch.from_numpy(meta).cuda(), torch.from_numpy(cidx).cuda(),
+                        R, K, V, M)
+    with pytest.raises(venom.VenomError) as e:
+        venom.decompress(x, check=True)
+    assert e.value.status == 7
+
+
+# ------------------------------------------------------------------ SpMM
+def oracle_problem(R, K, T, V, M, dt, seed, bias=False, kind="gauss"):
+    A = make_input(R, K, kind, dt, seed, M) if kind != "gauss" else synth.gaussian((R, K), 0.02, dt, seed)
+    B = synth.gaussian((K, T), 1.0, dt, seed + 1)
+    bv = synth.gaussian((R,), 0.5, dt, seed + 2) if bias else None
+    vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+    return A, B, bv, (vals, meta, cidx)
+
+
+def vnm_from(parts, R, K, V, M, dt):
+    vals, meta, cidx = parts
+    return venom.VNMTensor(to_dev(vals, dt), torch.from_numpy(meta).cuda(), torch.from_numpy(cidx).cuda(),
+                           R, K, V, M)
+
+
+def test_spmm_identity_probe_exact():
+    """P6: B = I_K => C == decompress(A) exactly (one product per output)."""
+    for (R, K, V, M, dt) in [(256, 256, 128, 8, F16), (128, 512, 64, 16, F16), (256, 256, 128, 4, BF16),
+                             (128, 320, 32, 10, F16)]:
+        A = synth.gaussian((R, K), 1.0, dt, 77)
+        vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+        D = oracle.decompress(vals, meta, cidx, R, K, dt, V, M)
+        I = to_dev(f64_to_bits(np.eye(K), dt), dt)
+        C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), I)
+        got = bits_to_f64(to_bits(C), dt)
+        assert np.array_equal(got, bits_to_f64(D, dt)), (R, K, V, M, dt)
+
+
+def test_spmm_one_hot_probes():
+    """One-hot B columns isolate single (row, group, position) entries: column t of B selects B row
+    k_t, so C[:, t] must equal column k_t of decompress(A) for every probe."""
+    R, K, V, M, dt = 128, 256, 128, 8, F16
+    A = synth.gaussian((R, K), 1.0, dt, 78)
+    vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+    D = bits_to_f64(oracle.decompress(vals, meta, cidx, R, K, dt, V, M), dt)
+    T = 64
+    ks = np.random.Generator(np.random.PCG64(5)).choice(K, size=T, replace=False)
+    Bm = np.zeros((K, T))
+    Bm[ks, np.arange(T)] = 1.0
+    C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), to_dev(f64_to_bits(Bm, dt), dt))
+    got = bits_to_f64(to_bits(C), dt)
+    assert np.array_equal(got, D[:, ks])
+
+
+SPMM_CASES = [
+    # R, K, T, V, M, dt, bias, tile_t
+    (128, 128, 128, 64, 8, F16, False, 0),     # configs[0]
+    (256, 512, 256, 128, 8, F16, True, 0),
+    (256, 512, 256, 128, 8, BF16, True, 0),
+    (384, 1024, 200, 128, 16, F16, False, 0),  # T tail, 3 row tiles
+    (192, 640, 136, 64, 40, F16, True, 0),     # odd number of 64-blocks (ragged last tile)
+    (256, 576, 96, 32, 36, F16, True, 0),      # V = 32
+    (256, 896, 128, 256, 28, BF16, False, 0),  # V = 256 (two 128-row slices share column_idx)
+    (256, 1600, 264, 128, 100, F16, True, 0),  # 2:100, K' tail (G = 16)
+    (512, 1024, 512, 128, 4, F16, True, 256),  # plain 2:4, tile 256
+    (512, 1024, 384, 128, 16, F16, True, 192),
+    (512, 2048, 256, 128, 32, BF16, False, 64),
+    (256, 1024, 256, 64, 8, F16, True, 128),   # V=64 tile 128 (single accumulator)
+    (128, 4096, 64, 128, 16, F16, False, 0),   # long K
+]
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,bias,tile_t", SPMM_CASES)
+def test_spmm_vs_oracle(R, K, T, V, M, dt, bias, tile_t):
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 500 + R + K + T + M, bias)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = vnm_from(parts, R, K, V, M, dt)
+    C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tile_t)
+    check_spmm(C, C_ref, dt)
+
+
+def test_spmm_ldb_ldc_views_and_shard_equality():
+    """B/C column slices through ldb/ldc (the multi-GPU T-split): each shard equals the matching
+    columns of the full product bit-for-bit (no split-K: same accumulation order)."""
+    R, K, T, V, M, dt = 256, 1024, 512, 128, 16, F16
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 900, True)
+    x = vnm_from(parts, R, K, V, M, dt)
+    Bd = to_dev(B, dt)
+    bias = to_dev(bv, dt)
+    full = venom.spmm(x, Bd, bias=bias)
+    Cbig = torch.zeros((R, T), dtype=tdt(dt), device="cuda")
+    for r in range(4):
+        sl = slice(r * T // 4, (r + 1) * T // 4)
+        venom.spmm(x, Bd[:, sl], bias=bias, out=Cbig[:, sl])
+    assert torch.equal(full.view(torch.int16), Cbig.view(torch.int16))
+    check_spmm(full, oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv), dt)
+
+
+def test_spmm_zero_A_gives_bias():
+    R, K, T, V, M, dt = 128, 256, 64, 64, 8, F16
+    A = np.zeros((R, K), np.uint16)
+    parts = oracle.compress(A, dt, V=V, M=M)
+    bv = synth.gaussian((R,), 1.0, dt, 3)
+    B = synth.gaussian((K, T), 1.0, dt, 4)
+    C = venom.spmm(vnm_from(parts, R, K, V, M, dt), to_dev(B, dt), bias=to_dev(bv, dt))
+    assert np.array_equal(to_bits(C), np.repeat(bv[:, None], T, axis=1))
+
+
+def test_spmm_gpu_compress_then_spmm_matches_library_gemm():
+    """End-to-end on the GPU path (compress -> spmm) vs the oracle, and vs cuBLAS on the
+    GPU-decompressed matrix (library pin)."""
+    R, K, T, V, M, dt = 512, 2048, 512, 128, 16, F16
+    A = synth.gaussian((R, K), 0.02, dt, 61)
+    B = synth.gaussian((K, T), 1.0, dt, 62)
+    x = venom.compress(to_dev(A, dt), V=V, M=M, check=True)
+    Bd = to_dev(B, dt)
+    C = venom.spmm(x, Bd)
+    parts = oracle.compress(A, dt, V=V, M=M)
+    check_spmm(C, oracle.spmm(*parts, R, K, dt, V, M, B), dt)
+    D = venom.decompress(x)
+    ref = (D.float() @ Bd.float()).double().cpu().numpy()
+    assert rel_fro(bits_to_f64(to_bits(C), dt), ref) <= TOL_FRO
+
+
+def test_spmm_reads_only_selected_rows():
+    """Rows of B that no block selects are poisoned with NaN: the output stays finite
+    (PAPER.md:231 'load only the rows of B selected by column-loc')."""
+    R, K, T, V, M, dt = 256, 1024, 128, 128, 16, F16
+    A, B, _, parts = oracle_problem(R, K, T, V, M, dt, 70)
+    cidx = parts[2]
+    used = set()
+    for rb in range(R // V):
+        for g in range(K // M):
+            used |= {g * M + int(c) for c in cidx[rb, g]}
+    Bp = B.copy()
+    for k in range(K):
+        if k not in used:
+            Bp[k] = 0x7E00
+    C = venom.spmm(vnm_from(parts, R, K, V, M, dt), to_dev(Bp, dt))
+    check_spmm(C, oracle.spmm(*parts, R, K, dt, V, M, B), dt)
+
+
+@pytest.mark.parametrize("wl", ["bert_large_ffn2_1024x4096x4096_64:2:8",
+                                "bert_large_ffn1_4096x1024x4096_64:2:8"])
+def test_spmm_full_size_bert_sampled(wl):
+    """BASELINE configs[1] at full size in the bench launch configuration: compressor bit-exact on
+    every element; SpMM checked on 64 sampled output columns (all rows) against the oracle."""
+    w = synth.WORKLOADS[wl]
+    R, K, T, V, M = w["R"], w["K"], w["T"], w["V"], w["M"]
+    sa, sb = synth.seeds(w["cfg"])
+    A = synth.gaussian((R, K), 0.02, F16, sa)
+    B = synth.gaussian((K, T), 1.0, F16, sb)
+    x, got = gpu_compress(A, F16, V, M)
+    parts = oracle.compress(A, F16, V=V, M=M)
+    for g, e in zip(got, parts):
+        assert np.array_equal(g.reshape(e.shape), e)
+    C = venom.spmm(x, to_dev(B, F16))
+    cols = np.random.Generator(np.random.PCG64(1)).choice(T, size=64, replace=False)
+    C_ref = oracle.spmm(*parts, R, K, F16, V, M, np.ascontiguousarray(B[:, cols]))
+    check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)

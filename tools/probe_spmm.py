@@ -1,0 +1,60 @@
+"""Diagnostics for layout bugs: runs tiny SpMMs with structured inputs and prints where the GPU
+result departs from the oracle (rows / columns / k-blocks). Not a test; output goes to stdout."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import oracle, synth
+import paper_2310_02065_b200 as venom
+from tests.helpers import bits_to_f64, f64_to_bits
+
+def dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.float16).cuda()
+
+def run(R, K, T, V, M, Akind, Bkind, tile_t=0):
+    if Akind == "ones":
+        A = f64_to_bits(np.ones((R, K)), 0)
+    elif Akind == "rowid":
+        A = f64_to_bits(np.repeat((np.arange(R) % 64 + 1.0)[:, None], K, 1), 0)
+    else:
+        A = synth.gaussian((R, K), 1.0, 0, 3)
+    if Bkind == "eye":
+        assert T == K
+        B = f64_to_bits(np.eye(K), 0)
+    elif Bkind == "rowid":
+        B = f64_to_bits(np.repeat((np.arange(K) % 16 + 1.0)[:, None], T, 1) / 16, 0)
+    else:
+        B = synth.gaussian((K, T), 1.0, 0, 4)
+    vals, meta, cidx = oracle.compress(A, 0, V=V, M=M)
+    ref = oracle.spmm(vals, meta, cidx, R, K, 0, V, M, B)
+    x = venom.VNMTensor(dev(vals), torch.from_numpy(meta).cuda(), torch.from_numpy(cidx).cuda(), R, K, V, M)
+    C = venom.spmm(x, dev(B), tile_t=tile_t)
+    torch.cuda.synchronize()
+    got = C.double().cpu().numpy()
+    bad = ~np.isclose(got, ref, rtol=2e-2, atol=1e-2)
+    print(f"== R{R} K{K} T{T} V{V} M{M} A={Akind} B={Bkind}: bad {bad.sum()}/{bad.size}")
+    if bad.any():
+        rows = np.nonzero(bad.any(1))[0]
+        cols = np.nonzero(bad.any(0))[0]
+        print("  bad rows:", rows[:40], "... n", len(rows))
+        print("  bad cols:", cols[:40], "... n", len(cols))
+        r = rows[0]
+        print("  row", r, "got", got[r, :8], "ref", ref[r, :8])
+        for rr in list(rows[:4]):
+            print("  row", rr, "got[:4]", np.round(got[rr, :4], 3), "ref[:4]", np.round(ref[rr, :4], 3))
+
+if __name__ == "__main__":
+    torch.cuda.init()
+    cases = [
+        (128, 128, 128, 128, 4, "ones", "eye"),
+        (128, 128, 128, 128, 4, "gauss", "eye"),
+        (128, 128, 64, 128, 4, "rowid", "rowid"),
+        (128, 256, 64, 128, 8, "gauss", "gauss"),
+        (128, 256, 256, 128, 8, "gauss", "eye"),
+        (128, 128, 128, 64, 8, "gauss", "gauss"),
+    ]
+    for c in cases:
+        try:
+            run(*c)
+        except Exception as e:
+            print("EXC", c, repr(e))
