@@ -152,14 +152,17 @@ __global__ void __launch_bounds__(256) vnm_compress_kernel(
     }
     const int64_t g = g0 + 2 * pp;
     uint16_t* vdst = values + (row * G + g) * 2;
+    const uint32_t w0 = static_cast<uint32_t>(out[0]) | (static_cast<uint32_t>(out[1]) << 16);
+    const uint32_t w1 = static_cast<uint32_t>(out[2]) | (static_cast<uint32_t>(out[3]) << 16);
     if (2 * pp + 1 < ng) {
-      // 8-byte aligned: (row*G + g) * 4 bytes with g even
-      *reinterpret_cast<uint2*>(vdst) =
-          make_uint2(static_cast<uint32_t>(out[0]) | (static_cast<uint32_t>(out[1]) << 16),
-                     static_cast<uint32_t>(out[2]) | (static_cast<uint32_t>(out[3]) << 16));
+      if (((row * G + g) & 1) == 0) {
+        *reinterpret_cast<uint2*>(vdst) = make_uint2(w0, w1);  // 8-byte aligned
+      } else {
+        reinterpret_cast<uint32_t*>(vdst)[0] = w0;  // odd G: only 4-byte aligned
+        reinterpret_cast<uint32_t*>(vdst)[1] = w1;
+      }
     } else {
-      *reinterpret_cast<uint32_t*>(vdst) =
-          static_cast<uint32_t>(out[0]) | (static_cast<uint32_t>(out[1]) << 16);
+      *reinterpret_cast<uint32_t*>(vdst) = w0;
     }
     metadata[row * meta_row + g / 2] = byte;
   }
