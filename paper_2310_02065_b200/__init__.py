@@ -130,7 +130,7 @@ def compressed_sizes(R: int, K: int, V: int, M: int, N: int = 2):
 
 
 def compress(A: torch.Tensor, V: int, M: int, N: int = 2, status: Optional[torch.Tensor] = None,
-             check: bool = False) -> VNMTensor:
+             check: bool = False, out: Optional[VNMTensor] = None) -> VNMTensor:
     """Magnitude V:N:M compression on the GPU. ``status`` (int32[1] on the
     device) receives data-dependent errors; ``check=True`` allocates one and synchronises to read
     it (raising on non-finite input)."""
@@ -138,9 +138,13 @@ def compress(A: torch.Tensor, V: int, M: int, N: int = 2, status: Optional[torch
     R, K = A.shape
     nv, nm, nc = compressed_sizes(R, K, V, M, N)
     G = K // M
-    values = torch.empty((R, G, 2), dtype=A.dtype, device=A.device)
-    metadata = torch.empty((R, (G + 1) // 2), dtype=torch.uint8, device=A.device)
-    column_idx = torch.empty((R // V, G, 4), dtype=torch.uint8, device=A.device)
+    if out is not None:
+        assert (out.R, out.K, out.V, out.M) == (R, K, V, M) and out.dtype == A.dtype
+        values, metadata, column_idx = out.values, out.metadata, out.column_idx
+    else:
+        values = torch.empty((R, G, 2), dtype=A.dtype, device=A.device)
+        metadata = torch.empty((R, (G + 1) // 2), dtype=torch.uint8, device=A.device)
+        column_idx = torch.empty((R // V, G, 4), dtype=torch.uint8, device=A.device)
     if check and status is None:
         status = torch.zeros(1, dtype=torch.int32, device=A.device)
     st = lib().venom_compress(ctypes.c_void_p(A.data_ptr()), R, K, A.stride(0), _dt(A.dtype),

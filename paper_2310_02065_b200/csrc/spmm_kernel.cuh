@@ -8,16 +8,17 @@
 //
 // B200 design:
 //   * persistent CTAs (one per SM), static round-robin tile schedule, tiles of 128 rows × BN cols;
-//   * warp 0  producer: column_idx words -> 4 B-row coordinates per group, TMA tile::gather4 of
-//             the selected rows (the paper's stage 1₂ "only the rows of B selected by column-loc")
-//             plus a TMA tile load of the compressed values; column_idx is register-prefetched
-//             several stages ahead (the paper's stage 1₁ "two-level pre-fetching");
-//   * warps 6-9 metadata: canonical per-row nibbles -> the tensor-core metadata layout in SMEM
-//             ("we also load directly ... the m-indices"), prefetched ahead;
-//   * warp 1  MMA: tcgen05.cp metadata SMEM->TMEM, tcgen05.mma.sp (M=128, N=BN, K=32) with fp32
+//   * warps 0..P-1 producers: column_idx words -> 4 B-row coordinates per group, TMA
+//             tile::gather4 of the selected rows (the paper's stage 1₂ "only the rows of B selected
+//             by column-loc") plus a TMA tile load of the compressed values; column_idx is
+//             register-prefetched several stages ahead (stage 1₁ "two-level pre-fetching"). TMA
+//             issue is serial per warp (~70 cycles per op, tools/microbench.cu), so P warps issue;
+//   * warp P  MMA: tcgen05.cp metadata SMEM->TMEM, tcgen05.mma.sp (M=128, N=BN, K=32) with fp32
 //             accumulation in TMEM (the paper's stage 2 on 5th-gen sparse tensor cores);
-//   * warps 2-5 epilogue: tcgen05.ld -> +bias -> round -> 16-byte global stores (stage 3),
-//             overlapped with the next tile's main loop when TMEM allows two accumulators.
+//   * warps P+1..P+4 epilogue: tcgen05.ld -> +bias -> round -> 16-byte global stores (stage 3),
+//             overlapped with the next tile's main loop when TMEM allows two accumulators;
+//   * warps P+5..P+8 metadata: canonical per-row nibbles -> the tensor-core metadata layout in
+//             SMEM ("we also load directly ... the m-indices"), prefetched ahead.
 // V = 128·k uses one V-block per tile; V ∈ {32, 64} packs NB = 128/V blocks into one 128-row A
 // tile and issues one MMA per block (each block has its own gathered B' and accumulator).
 #pragma once
@@ -45,11 +46,12 @@ struct SpmmParams {
   int is_bf16;
 };
 
-template <int NB_, int BN_, int STAGES_>
+template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8>
 struct SpmmCfg {
   static constexpr int NB = NB_;              // V-blocks per 128-row tile
   static constexpr int BN = BN_;              // output columns per tile (MMA N)
   static constexpr int STAGES = STAGES_;
+  static constexpr int P = PRODUCERS_;        // gather-issuing warps (TMA issue is per-warp serial)
   static constexpr int BM = 128;              // MMA M
   static constexpr int KG = 32;               // groups per k-stage: K' = 128, 4 MMAs of K = 32
   static constexpr int A_BYTES = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
@@ -62,7 +64,14 @@ struct SpmmCfg {
   static constexpr int E_COLS = 8;            // two 4-column metadata regions
   static constexpr int ACC_BUFS = (2 * ACC_COLS + E_COLS <= 512) ? 2 : 1;
   static constexpr int E_COL = 512 - E_COLS;
-  static constexpr int NUM_THREADS = 320;
+  static constexpr int NCH = BN / 64;         // 64-column chunks of B' per block
+  static constexpr int NOPS = NB * NCH * 32;  // gather4 ops per stage (one per group × chunk × block)
+  static constexpr int OPS_PER_WARP = NOPS / P;
+  static constexpr int LANE_OPS = (OPS_PER_WARP + 31) / 32;
+  // warp roles: [0,P) producers, P MMA, P+1..P+4 epilogue, P+5..P+8 metadata
+  static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 5;
+  static constexpr int NUM_THREADS = 32 * (P + 9);
+  static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
   static constexpr int BAR_BYTES = 256;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
@@ -146,7 +155,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     prefetch_tmap(&tm_values);
     prefetch_tmap(&tm_b);
   }
-  if (warp == 1) tmem_alloc<512>(smem_u32(tmem_base_slot));
+  if (warp == Cfg::W_MMA) tmem_alloc<512>(smem_u32(tmem_base_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -170,28 +179,43 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     return rb < nrb ? rb : nrb - 1;  // padding block of a ragged last tile: any valid block
   };
 
-  if (warp == 0) {
-    // ======================= producer: values tile + gathered B' rows =======================
+  if (warp < Cfg::P) {
+    // ======================= producers: values tile + gathered B' rows =======================
+    // Stage ops are (block b, chunk c, group q); warp w issues ops [w·OPS_PER_WARP, ...), one per
+    // lane: TMA issue is serial within a warp, so the gathers are spread over P warps.
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
-    uint32_t cw[kPrefetch][NB];
-    auto fetch = [&](int it, uint32_t (&w)[NB]) {
+    uint32_t cw[kPrefetch][Cfg::LANE_OPS];
+    auto op_of = [&](int j, int& b, int& c, int& q) -> bool {
+      const int o_local = lane + 32 * j;
+      if (o_local >= Cfg::OPS_PER_WARP) return false;
+      const int o = warp * Cfg::OPS_PER_WARP + o_local;
+      b = o / (Cfg::NCH * 32);
+      c = (o / 32) % Cfg::NCH;
+      q = o % 32;
+      return true;
+    };
+    auto fetch = [&](int it, uint32_t (&w)[Cfg::LANE_OPS]) {
       if (it >= total) return;
       int m_tile, n_tile;
       tile_of(it / p.num_ks, m_tile, n_tile);
-      const int gg = (it % p.num_ks) * Cfg::KG + lane;
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
-        w[b] = (gg < p.G) ? __ldg(reinterpret_cast<const uint32_t*>(p.column_idx) +
-                                  static_cast<int64_t>(block_of(m_tile, b)) * p.G + gg)
-                          : 0u;
+      for (int j = 0; j < Cfg::LANE_OPS; ++j) {
+        int b, c, q;
+        w[j] = 0u;
+        if (!op_of(j, b, c, q)) continue;
+        const int gg = (it % p.num_ks) * Cfg::KG + q;
+        if (gg < p.G)
+          w[j] = __ldg(reinterpret_cast<const uint32_t*>(p.column_idx) +
+                       static_cast<int64_t>(block_of(m_tile, b)) * p.G + gg);
+      }
     };
 #pragma unroll
     for (int j = 0; j < kPrefetch; ++j) fetch(j, cw[j]);
     for (int it0 = 0; it0 < total; it0 += kPrefetch) {
 #pragma unroll
-      for (int j = 0; j < kPrefetch; ++j) {
-        const int it = it0 + j;
+      for (int jj = 0; jj < kPrefetch; ++jj) {
+        const int it = it0 + jj;
         if (it < total) {
           const int stage = it % STAGES;
           const uint32_t phase = (it / STAGES) & 1;
@@ -200,32 +224,30 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           const int ks = it % p.num_ks;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
-          if (lane == 0) {
+          if (warp == 0 && lane == 0) {
             mbar_arrive_expect_tx(full0 + 8 * stage, Cfg::TX_BYTES);
             tma_load_2d(sbase, &tm_values, full0 + 8 * stage, ks * 64, m_tile * 128, pol_a);
           }
-          __syncwarp();
-          const int gg = ks * Cfg::KG + lane;
           const int col0 = n_tile * BN;
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
+          for (int j = 0; j < Cfg::LANE_OPS; ++j) {
+            int b, c, q;
+            if (!op_of(j, b, c, q)) continue;
+            const int gg = ks * Cfg::KG + q;
+            const uint32_t w = cw[jj][j];
             int r[4];
-            const uint32_t w = cw[j][b];
 #pragma unroll
             for (int t = 0; t < 4; ++t)
               r[t] = (gg < p.G) ? gg * p.M + static_cast<int>((w >> (8 * t)) & 0xFF)
                                 : static_cast<int>(p.K);  // past the last row: zero fill
-            const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + lane * 512;
-#pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_gather4(bdst + c * Cfg::B_CHUNK, &tm_b, full0 + 8 * stage, col0 + 64 * c, r[0],
-                          r[1], r[2], r[3], pol_b);
+            const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK + q * 512;
+            tma_gather4(bdst, &tm_b, full0 + 8 * stage, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
           }
-          fetch(it + kPrefetch, cw[j]);
+          fetch(it + kPrefetch, cw[jj]);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == Cfg::W_MMA) {
     // ======================= MMA issuer (one elected lane) =======================
     constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128, BN);
     for (int tl = 0; tl < my_tiles; ++tl) {
@@ -266,7 +288,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
         __syncwarp();
       }
     }
-  } else if (warp >= 2 && warp <= 5) {
+  } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 4) {
     // ======================= epilogue: TMEM -> +bias -> round -> global =======================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r_local = 32 * q + lane;
@@ -314,7 +336,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     // ======================= metadata: canonical nibbles -> tensor-core layout =======================
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
     // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3.
-    const int L = 32 * (warp - 6) + lane;
+    const int L = 32 * (warp - Cfg::W_META) + lane;
     const int m_a = (L & 7) + 16 * (L >> 4);
     const int k1 = (L >> 3) & 1;
     uint32_t wa[kPrefetch][4], wb[kPrefetch][4];
@@ -353,7 +375,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == Cfg::W_MMA) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
   }
