@@ -190,6 +190,8 @@ def run_gpu(args, ws, rank, local):
         kw["tile_t"] = args.tile_t
     if args.stages:
         kw["stages"] = args.stages
+    if args.strategy:
+        kw["strategy"] = {"gather": 1, "densek": 2}[args.strategy]
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
 
@@ -420,6 +422,8 @@ def main(argv=None):
     ap.add_argument("--step", choices=["full", "spmm"], default="full")
     ap.add_argument("--tile-t", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--strategy", choices=["gather", "densek"], default=None,
+                    help="force a venom_spmm strategy (default: the library's cost model)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

@@ -102,8 +102,11 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  *   C     dtype[R][ldc] row-major
  *   bias  nullable dtype[R], added in fp32 before rounding
  * Requirements (else VENOM_ERR_UNSUPPORTED_PATTERN / INVALID_ARGUMENT):
- *   V in {32, 64} or V % 128 == 0, V | R; M in [4,256], M | K; G = K/M with G % 4 == 0;
- *   T % 8 == 0, ldb % 8 == 0, ldc % 8 == 0, ldb >= T, ldc >= T; values/B/C 16-byte aligned.
+ *   V | R; M in [4,256], M | K; T % 8 == 0, ldb % 8 == 0, ldc % 8 == 0, ldb >= T, ldc >= T;
+ *   values/B/C 16-byte aligned; and at least one strategy applies:
+ *     gather : V in {32, 64} or V % 128 == 0, and G = K/M with G % 4 == 0
+ *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
+ *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
  * Metadata validity is NOT checked here (use venom_decompress with dev_status to validate);
  * malformed metadata gives undefined values, never out-of-bounds accesses.
  */
@@ -114,12 +117,20 @@ venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uin
                           const void* bias,
                           venom_dtype_t dt, venom_stream_t stream);
 
-/* Optional tile override for venom_spmm (benchmarking / tuning). Zero fields = library default.
- * tile_t: output columns per CTA tile (64, 128 or 256); stages: pipeline depth. */
+/* Optional overrides for venom_spmm (benchmarking / tuning / ablation). Zero = library default.
+ *   tile_t    output columns per CTA tile (64, 128, 192 or 256; availability depends on strategy)
+ *   stages    pipeline depth (where a variant exists)
+ *   max_ctas  persistent grid cap (0 = #SMs)
+ *   strategy  VENOM_STRATEGY_AUTO: cost model; GATHER: the paper's mapping (gather the 4 selected
+ *             B rows per group through column_idx, 2:4 MMA over K' = 4K/M); DENSE_K: expand the
+ *             V:N:M operand on the fly to 2:4 over the original K and use dense B tiles (requires
+ *             M in {4,8,16,32}, G % 4 == 0). Both return the same product. */
+enum { VENOM_STRATEGY_AUTO = 0, VENOM_STRATEGY_GATHER = 1, VENOM_STRATEGY_DENSE_K = 2 };
 typedef struct {
   int32_t tile_t;
   int32_t stages;
-  int32_t max_ctas;  /* persistent grid cap (0 = #SMs) */
+  int32_t max_ctas;
+  int32_t strategy;
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

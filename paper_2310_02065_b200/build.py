@@ -2,6 +2,7 @@
 it travels with the repository snapshot to the GPU box."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -10,8 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libvenom.so")
 SOURCES = [os.path.join(HERE, "csrc", "venom_api.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("ptx_sm100.cuh", "format_kernels.cuh",
-                                                          "spmm_kernel.cuh")] + \
+DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
     [os.path.join(ROOT, "include", "venom.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -4,6 +4,24 @@
 #pragma once
 #include <cstdint>
 
+// Optional pipeline tracing (tools/trace_kernels.cu builds with -DVENOM_TRACE): per event kind and
+// k-stage iteration, CTA 0/1 record %globaltimer. Compiled out of libvenom.so.
+#ifdef VENOM_TRACE
+__device__ unsigned long long* g_venom_trace;
+#define VENOM_TRACE_EVENT(kind, it)                                                         \
+  do {                                                                                      \
+    if (blockIdx.x < 2 && (it) < 256) {                                                     \
+      unsigned long long t_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_venom_trace[(blockIdx.x * 16 + (kind)) * 256 + (it)] = t_;                          \
+    }                                                                                       \
+  } while (0)
+#else
+#define VENOM_TRACE_EVENT(kind, it) \
+  do {                              \
+  } while (0)
+#endif
+
 namespace venom {
 namespace ptx {
 

@@ -33,17 +33,19 @@
 namespace venom {
 
 struct SpmmParams {
+  const uint16_t* values;   // read directly by the dense-K expanders (the gathered kernel uses TMA)
   const uint8_t* metadata;
   const uint8_t* column_idx;
   const uint16_t* bias;
   uint16_t* C;
   int64_t R, K, T, ldc;
   int V, M, G, meta_row;
-  int num_ks;    // k-stages per tile = ceil(G / 32)
+  int num_ks;    // k-stages per tile: ceil(G / 32) gathered, ceil(K / 128) dense-K
   int m_tiles;   // ceil(R / 128)
   int n_tiles;   // ceil(T / BN)
   int num_tiles;
   int is_bf16;
+  int dbg;  // debug/ablation flags (0 in production)
 };
 
 template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8>
@@ -120,6 +122,118 @@ __device__ __forceinline__ void load_meta_stage(const SpmmParams& p, int64_t row
   }
 }
 
+// Persistent static schedule: CTA b runs tiles b, b + grid, b + 2·grid, ... in T-band order (all
+// row tiles of one column band first, so concurrently running CTAs share the B column slab in L2).
+__device__ __forceinline__ void tile_coords(const SpmmParams& p, int tl, int& m_tile, int& n_tile) {
+  const int t = static_cast<int>(blockIdx.x) + tl * static_cast<int>(gridDim.x);
+  n_tile = t / p.m_tiles;
+  m_tile = t - n_tile * p.m_tiles;
+}
+
+// MMA issuer (one elected lane of one warp): per k-stage, copy the stage's metadata SMEM->TMEM
+// (tcgen05.cp, 128 lanes × 4 words) and issue 4 sparse MMAs (K = 32 each) per V-block.
+// Stage layout (both kernels): [A 16 KB K-major SW128][NB × B' (BN/64 chunks × 16 KB, MN-major
+// SW128)][metadata 2 KB: lane L at 16·L].
+template <class Cfg, bool kBF16>
+__device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
+                                         uint32_t smem0, uint32_t full0, uint32_t empty0,
+                                         uint32_t accf0, uint32_t acce0, int lane) {
+  using namespace ptx;
+  constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
+  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128, BN);
+  for (int tl = 0; tl < my_tiles; ++tl) {
+    const int ab = tl % Cfg::ACC_BUFS;
+    const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
+    mbar_wait(acce0 + 8 * ab, aphase ^ 1);
+    tc_fence_after();
+    const uint32_t d_tile = tmem_base + ab * Cfg::ACC_COLS;
+    for (int ks = 0; ks < p.num_ks; ++ks) {
+      const int it = tl * p.num_ks + ks;
+      const int stage = it % STAGES;
+      mbar_wait(full0 + 8 * stage, (it / STAGES) & 1);
+      tc_fence_after();
+      if (lane == 0) VENOM_TRACE_EVENT(1, it);
+      if (lane == 0) {
+        const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
+        const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * (it & 1);
+        // metadata: 128 rows × 16 B, core matrices of 8 rows contiguous (SBO = 128 B)
+        tc_cp_128x128b(e_tmem, smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0));
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          const uint32_t e_addr = e_tmem + kb;
+          const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
+          // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
+          const uint64_t adesc = smem_desc(sbase + kb * 32, 16, 1024, 2);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
+            // K advance 32 rows = 4096 B per MMA
+            const uint64_t bdesc =
+                smem_desc(sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + kb * 4096, Cfg::B_CHUNK, 1024, 2);
+            tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
+                          (ks | kb) != 0 ? 1u : 0u);
+          }
+        }
+        tc_commit(empty0 + 8 * stage);
+        if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
+        VENOM_TRACE_EVENT(2, it);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Epilogue (4 warps, one TMEM lane quarter each): TMEM -> +bias (fp32) -> RNE to fp16/bf16 ->
+// 16-byte global stores; releases the accumulator buffer to the MMA warp.
+template <class Cfg, bool kBF16>
+__device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
+                                              uint32_t accf0, uint32_t acce0, int warp, int lane) {
+  using namespace ptx;
+  constexpr int NB = Cfg::NB, BN = Cfg::BN;
+  const int q = warp & 3;  // TMEM lane quarter this warp may access
+  const int r_local = 32 * q + lane;
+  for (int tl = 0; tl < my_tiles; ++tl) {
+    int m_tile, n_tile;
+    tile_coords(p, tl, m_tile, n_tile);
+    const int ab = tl % Cfg::ACC_BUFS;
+    mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
+    tc_fence_after();
+    const int64_t row = static_cast<int64_t>(m_tile) * 128 + r_local;
+    const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
+    const float bv = (p.bias != nullptr && row < p.R)
+                         ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
+                                  : __half2float(__ushort_as_half(p.bias[row])))
+                         : 0.0f;
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
+                           ab * Cfg::ACC_COLS + b * BN;
+    const int64_t col_base = static_cast<int64_t>(n_tile) * BN;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_row + 32 * c, v);
+      tmem_ld_wait();
+      const int64_t col = col_base + 32 * c;
+      if (row < p.R) {
+        uint16_t* dst = p.C + row * p.ldc + col;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (col + 8 * u < p.T) {
+            uint4 o;
+            o.x = pack2<kBF16>(__uint_as_float(v[8 * u + 0]) + bv, __uint_as_float(v[8 * u + 1]) + bv);
+            o.y = pack2<kBF16>(__uint_as_float(v[8 * u + 2]) + bv, __uint_as_float(v[8 * u + 3]) + bv);
+            o.z = pack2<kBF16>(__uint_as_float(v[8 * u + 4]) + bv, __uint_as_float(v[8 * u + 5]) + bv);
+            o.w = pack2<kBF16>(__uint_as_float(v[8 * u + 6]) + bv, __uint_as_float(v[8 * u + 7]) + bv);
+            *reinterpret_cast<uint4*>(dst + 8 * u) = o;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acce0 + 8 * ab);
+  }
+}
+
 template <class Cfg, bool kBF16>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
@@ -169,11 +283,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   const int total = my_tiles * p.num_ks;  // k-stage iterations this CTA runs
   const int nrb = static_cast<int>(p.R / p.V);
 
-  auto tile_of = [&](int tl, int& m_tile, int& n_tile) {
-    const int t = static_cast<int>(blockIdx.x) + tl * static_cast<int>(gridDim.x);
-    n_tile = t / p.m_tiles;  // T-band order: all row tiles of one column band first
-    m_tile = t - n_tile * p.m_tiles;
-  };
+  auto tile_of = [&](int tl, int& m_tile, int& n_tile) { tile_coords(p, tl, m_tile, n_tile); };
   auto block_of = [&](int m_tile, int b) -> int {
     const int rb = (NB == 1) ? (m_tile * 128) / p.V : m_tile * NB + b;
     return rb < nrb ? rb : nrb - 1;  // padding block of a ragged last tile: any valid block
@@ -248,90 +358,9 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
       }
     }
   } else if (warp == Cfg::W_MMA) {
-    // ======================= MMA issuer (one elected lane) =======================
-    constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128, BN);
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      const int ab = tl % Cfg::ACC_BUFS;
-      const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
-      mbar_wait(acce0 + 8 * ab, aphase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tile = tmem_base + ab * Cfg::ACC_COLS;
-      for (int ks = 0; ks < p.num_ks; ++ks) {
-        const int it = tl * p.num_ks + ks;
-        const int stage = it % STAGES;
-        mbar_wait(full0 + 8 * stage, (it / STAGES) & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
-          const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * (it & 1);
-          // metadata: 128 rows × 16 B, core matrices of 8 rows contiguous (SBO = 128 B)
-          tc_cp_128x128b(e_tmem, smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0));
-#pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {
-            const uint32_t e_addr = e_tmem + kb;
-            const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
-            // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
-            const uint64_t adesc = smem_desc(sbase + kb * 32, 16, 1024, 2);
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
-              // K advance 32 rows = 4096 B per MMA
-              const uint64_t bdesc =
-                  smem_desc(sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + kb * 4096, Cfg::B_CHUNK, 1024, 2);
-              tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
-                            (ks | kb) != 0 ? 1u : 0u);
-            }
-          }
-          tc_commit(empty0 + 8 * stage);
-          if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
-        }
-        __syncwarp();
-      }
-    }
+    mma_role<Cfg, kBF16>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 4) {
-    // ======================= epilogue: TMEM -> +bias -> round -> global =======================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int r_local = 32 * q + lane;
-    for (int tl = 0; tl < my_tiles; ++tl) {
-      int m_tile, n_tile;
-      tile_of(tl, m_tile, n_tile);
-      const int ab = tl % Cfg::ACC_BUFS;
-      mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
-      tc_fence_after();
-      const int64_t row = static_cast<int64_t>(m_tile) * 128 + r_local;
-      const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
-      const float bv = (p.bias != nullptr && row < p.R)
-                           ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
-                                    : __half2float(__ushort_as_half(p.bias[row])))
-                           : 0.0f;
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
-                             ab * Cfg::ACC_COLS + b * BN;
-      const int64_t col_base = static_cast<int64_t>(n_tile) * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + 32 * c, v);
-        tmem_ld_wait();
-        const int64_t col = col_base + 32 * c;
-        if (row < p.R) {
-          uint16_t* dst = p.C + row * p.ldc + col;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (col + 8 * u < p.T) {
-              uint4 o;
-              o.x = pack2<kBF16>(__uint_as_float(v[8 * u + 0]) + bv, __uint_as_float(v[8 * u + 1]) + bv);
-              o.y = pack2<kBF16>(__uint_as_float(v[8 * u + 2]) + bv, __uint_as_float(v[8 * u + 3]) + bv);
-              o.z = pack2<kBF16>(__uint_as_float(v[8 * u + 4]) + bv, __uint_as_float(v[8 * u + 5]) + bv);
-              o.w = pack2<kBF16>(__uint_as_float(v[8 * u + 6]) + bv, __uint_as_float(v[8 * u + 7]) + bv);
-              *reinterpret_cast<uint4*>(dst + 8 * u) = o;
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acce0 + 8 * ab);
-    }
+    epilogue_role<Cfg, kBF16>(p, my_tiles, tmem_base, accf0, acce0, warp, lane);
   } else {
     // ======================= metadata: canonical nibbles -> tensor-core layout =======================
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high

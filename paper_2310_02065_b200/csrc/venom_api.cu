@@ -5,14 +5,17 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/venom.h"
 #include "format_kernels.cuh"
+#include "densek_kernel.cuh"
 #include "spmm_kernel.cuh"
 
 namespace {
 
+using venom::DenseKCfg;
 using venom::SpmmCfg;
 using venom::SpmmParams;
 
@@ -83,6 +86,69 @@ venom_status_t run_spmm_dt(bool bf16, const CUtensorMap& tv, const CUtensorMap& 
                            int max_ctas, cudaStream_t s) {
   return bf16 ? run_spmm<Cfg, true>(tv, tb, p, max_ctas, s)
               : run_spmm<Cfg, false>(tv, tb, p, max_ctas, s);
+}
+
+template <class Cfg, bool kBF16>
+venom_status_t run_densek(const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p, int max_ctas,
+                          cudaStream_t s) {
+  // compressed values: 2-D [R rows][2G] 16-bit, box VE × 128 rows (one k-stage), no swizzle
+  CUtensorMap tv;
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * p.G), static_cast<cuuint64_t>(p.R)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(4 * static_cast<int64_t>(p.G))};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(Cfg::VE), 128};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(p.values), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  }
+  auto kern = venom::vnm_spmm_densek_kernel<Cfg, kBF16>;
+  const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return VENOM_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid < 1) return VENOM_OK;
+  kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tb, tv, p);
+  return launch_status();
+}
+
+template <int BN, int ST>
+venom_status_t run_densek_m(int M, bool bf16, const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p,
+                            int max_ctas, cudaStream_t s) {
+#define VENOM_DK(MM)                                                                      \
+  case MM:                                                                                \
+    return bf16 ? run_densek<DenseKCfg<BN, ST, MM>, true>(tb, enc, p, max_ctas, s)        \
+                : run_densek<DenseKCfg<BN, ST, MM>, false>(tb, enc, p, max_ctas, s);
+  switch (M) {
+    VENOM_DK(4) VENOM_DK(8) VENOM_DK(16) VENOM_DK(32)
+  }
+#undef VENOM_DK
+  return VENOM_ERR_UNSUPPORTED_PATTERN;
+}
+
+// Cost model: both strategies are bound by max(tensor time, L2->SMEM
+// feed time) with the feed rates measured by tools/microbench.cu on B200 (gather of 128-byte rows
+// ~31 B/cycle/SM; 16 KB TMA boxes ~55 B/cycle/SM) and the sparse MMA issue rate (~13k dense-
+// equivalent FLOP/cycle/SM at N = 256). Returns relative costs in cycles·SM.
+double cost_gather(int64_t R, int64_t K, int64_t T, int V, int M, int bn) {
+  const double G = double(K / M), Kp = 4.0 * G;
+  const int NB = (V % 128 == 0) ? 1 : 128 / V;
+  const double mtiles = double((R + 127) / 128), ntiles = double((T + bn - 1) / bn);
+  const double bytes = mtiles * NB * Kp * double(T) * 2.0 + double(R) * 2.0 * G * 2.0 * ntiles;
+  const double mma = mtiles * NB * 2.0 * 128.0 * Kp * double(T);
+  return bytes / 31.0 > mma / 13000.0 ? bytes / 31.0 : mma / 13000.0;
+}
+double cost_densek(int64_t R, int64_t K, int64_t T, int M, int bn) {
+  const double G = double(K / M);
+  const double mtiles = double((R + 127) / 128), ntiles = double((T + bn - 1) / bn);
+  const double bytes = mtiles * double(K) * double(T) * 2.0 + double(R) * G * 4.5 * ntiles;
+  const double mma = mtiles * 2.0 * 128.0 * double(K) * double(T);
+  return bytes / 55.0 > mma / 13000.0 ? bytes / 55.0 : mma / 13000.0;
 }
 
 }  // namespace
@@ -189,9 +255,14 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (st != VENOM_OK) return st;
   if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
   const int V = f.v;
-  if (!(V == 32 || V == 64 || V % 128 == 0)) return VENOM_ERR_UNSUPPORTED_PATTERN;
   const int64_t G = K / f.m;
-  if (G % 4 != 0) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  const bool can_gather = (V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0);
+  const bool can_densek = (f.m % 4 == 0) && (f.m <= 32) && (G % 4 == 0);
+  const int strategy = opts ? opts->strategy : VENOM_STRATEGY_AUTO;
+  if (strategy == VENOM_STRATEGY_GATHER && !can_gather) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (strategy == VENOM_STRATEGY_DENSE_K && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (strategy < 0 || strategy > 2) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!can_gather && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (T < 0 || ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
     return VENOM_ERR_INVALID_ARGUMENT;
   if (R == 0 || T == 0) return VENOM_OK;
@@ -217,10 +288,65 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   EncodeTiledFn enc = encode_fn();
   if (!enc) return VENOM_ERR_CUDA;
   const int NB = (V % 128 == 0) ? 1 : 128 / V;
-  int tile_t = opts && opts->tile_t ? opts->tile_t : (NB == 1 ? 128 : (NB == 2 ? 64 : 64));
-  int stages = opts && opts->stages ? opts->stages : 0;
   const int max_ctas = opts ? opts->max_ctas : 0;
+  const int stages = opts ? opts->stages : 0;
+  int tile_t = opts ? opts->tile_t : 0;
 
+  bool use_densek;
+  if (strategy == VENOM_STRATEGY_GATHER) use_densek = false;
+  else if (strategy == VENOM_STRATEGY_DENSE_K) use_densek = true;
+  else if (!can_gather) use_densek = true;
+  else if (!can_densek) use_densek = false;
+  else use_densek = cost_densek(R, K, T, f.m, 256) < cost_gather(R, K, T, V, f.m, NB == 1 ? 256 : 128);
+
+  SpmmParams p;
+  p.values = static_cast<const uint16_t*>(values);
+  p.metadata = metadata;
+  p.column_idx = column_idx;
+  p.bias = static_cast<const uint16_t*>(bias);
+  p.C = static_cast<uint16_t*>(C);
+  p.R = R;
+  p.K = K;
+  p.T = T;
+  p.ldc = ldc;
+  p.V = V;
+  p.M = f.m;
+  p.G = static_cast<int>(G);
+  p.meta_row = static_cast<int>((G + 1) / 2);
+  p.m_tiles = static_cast<int>((R + 127) / 128);
+  p.is_bf16 = bf16;
+  {
+    const char* d = getenv("VENOM_DEBUG_FLAGS");
+    p.dbg = d ? atoi(d) : 0;
+  }
+  auto set_tiles = [&](int bn) {
+    p.n_tiles = static_cast<int>((T + bn - 1) / bn);
+    p.num_tiles = p.m_tiles * p.n_tiles;
+  };
+
+  auto encode_b = [&](CUtensorMap* tb, cuuint32_t box_rows) -> bool {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(K)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldb)};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(tb, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(B), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+
+  if (use_densek) {
+    // B: 2-D [K rows][T], box 64 columns × 128 rows (one K-stage of one 64-column chunk), SW128
+    CUtensorMap tb;
+    if (!encode_b(&tb, 128)) return VENOM_ERR_CUDA;
+    p.num_ks = static_cast<int>((K + 127) / 128);
+    if (tile_t == 0) tile_t = 256;
+    set_tiles(tile_t);
+    if (tile_t == 256) return run_densek_m<256, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
+    if (tile_t == 128) return run_densek_m<128, 3>(f.m, bf16, tb, enc, p, max_ctas, s);
+    return VENOM_ERR_INVALID_ARGUMENT;
+  }
+
+  // gathered strategy
   // values: 2-D [R rows][2G] 16-bit, box 64 × 128 rows, 128B swizzle (UMMA K-major SW128)
   CUtensorMap tv, tb;
   {
@@ -234,38 +360,9 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
       return VENOM_ERR_CUDA;
   }
   // B: 2-D [K rows][T] 16-bit, box 64 × 1 row (gather4 fetches 4 rows), 128B swizzle
-  {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(K)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldb)};
-    cuuint32_t box[2] = {64, 1};
-    cuuint32_t es[2] = {1, 1};
-    if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(B), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return VENOM_ERR_CUDA;
-  }
-
-  SpmmParams p;
-  p.metadata = metadata;
-  p.column_idx = column_idx;
-  p.bias = static_cast<const uint16_t*>(bias);
-  p.C = static_cast<uint16_t*>(C);
-  p.R = R;
-  p.K = K;
-  p.T = T;
-  p.ldc = ldc;
-  p.V = V;
-  p.M = f.m;
-  p.G = static_cast<int>(G);
-  p.meta_row = static_cast<int>((G + 1) / 2);
+  if (!encode_b(&tb, 1)) return VENOM_ERR_CUDA;
   p.num_ks = static_cast<int>((G + 31) / 32);
-  p.m_tiles = static_cast<int>((R + 127) / 128);
-  p.is_bf16 = bf16;
-
-  auto set_tiles = [&](int bn) {
-    p.n_tiles = static_cast<int>((T + bn - 1) / bn);
-    p.num_tiles = p.m_tiles * p.n_tiles;
-  };
+  if (tile_t == 0) tile_t = (NB == 1) ? 256 : (NB == 2 ? 128 : 64);
   set_tiles(tile_t);
   if (NB == 1) {
     if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2>>(bf16, tv, tb, p, max_ctas, s);

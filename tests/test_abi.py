@@ -60,8 +60,9 @@ def _spmm(L, R=256, K=512, V=128, M=8, T=64, ldb=64, ldc=64, n=2, dt=0):
 
 
 def test_spmm_argument_errors(L):
-    assert _spmm(L, R=384, V=96) == 4          # V not in {32,64} ∪ 128N
-    assert _spmm(L, K=8 * 6, M=8) == 4         # G = 6, not a multiple of 4
+    assert _spmm(L, R=384, V=96, K=640, M=10) == 4   # gather: V not in {32,64} ∪ 128N; dense-K: M ∤ 128
+    assert _spmm(L, K=12 * 6, M=12) == 4       # gather: G = 6 not a multiple of 4; dense-K: M = 12
+    assert _spmm(L, K=8 * 6, M=8) == 4         # G = 6: neither strategy (TMA row stride 4G % 16)
     assert _spmm(L, T=60, ldb=64, ldc=64) == 1  # T % 8
     assert _spmm(L, ldb=32) == 1               # ldb < T
     assert _spmm(L, ldc=68) == 1               # ldc % 8

@@ -204,13 +204,60 @@ SPMM_CASES = [
 ]
 
 
+def strategies(K, V, M):
+    """Strategies applicable to a problem (include/venom.h): AUTO plus each forced one."""
+    out = [venom.STRATEGY_AUTO]
+    if (V in (32, 64) or V % 128 == 0) and (K // M) % 4 == 0:
+        out.append(venom.STRATEGY_GATHER)
+    if M in (4, 8, 16, 32) and (K // M) % 4 == 0:
+        out.append(venom.STRATEGY_DENSE_K)
+    return out
+
+
 @pytest.mark.parametrize("R,K,T,V,M,dt,bias,tile_t", SPMM_CASES)
 def test_spmm_vs_oracle(R, K, T, V, M, dt, bias, tile_t):
     A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 500 + R + K + T + M, bias)
     C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
     x = vnm_from(parts, R, K, V, M, dt)
-    C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tile_t)
-    check_spmm(C, C_ref, dt)
+    for strat in strategies(K, V, M):
+        tt = tile_t if strat != venom.STRATEGY_DENSE_K or tile_t in (0, 128, 256) else 0
+        C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tt,
+                       strategy=strat)
+        check_spmm(C, C_ref, dt)
+
+
+DENSEK_CASES = [
+    # R, K, T, V, M, dt, bias — dense-K only shapes: any V, K not a multiple of 128, M = 4 .. 32
+    (128, 224, 64, 16, 8, F16, True),
+    (96, 384, 40, 1, 4, F16, False),
+    (256, 512, 136, 8, 16, BF16, True),
+    (384, 1280, 256, 128, 32, F16, True),
+    (200, 640, 72, 40, 32, F16, False),
+    (256, 1088, 512, 64, 16, BF16, True),
+    (128, 4096, 64, 128, 4, F16, True),
+]
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,bias", DENSEK_CASES)
+def test_spmm_densek_vs_oracle(R, K, T, V, M, dt, bias):
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 700 + R + K + T + M, bias)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = vnm_from(parts, R, K, V, M, dt)
+    for tt in (0, 128):
+        C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tt,
+                       strategy=venom.STRATEGY_DENSE_K)
+        check_spmm(C, C_ref, dt)
+
+
+def test_spmm_identity_probe_exact_densek():
+    """P6 through the dense-K strategy: B = I => C == decompress(A) exactly."""
+    for (R, K, V, M, dt) in [(256, 256, 128, 8, F16), (128, 512, 16, 16, F16), (256, 256, 64, 4, BF16)]:
+        A = synth.gaussian((R, K), 1.0, dt, 79)
+        vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+        D = oracle.decompress(vals, meta, cidx, R, K, dt, V, M)
+        I = to_dev(f64_to_bits(np.eye(K), dt), dt)
+        C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), I, strategy=venom.STRATEGY_DENSE_K)
+        assert np.array_equal(bits_to_f64(to_bits(C), dt), bits_to_f64(D, dt)), (R, K, V, M, dt)
 
 
 def test_spmm_ldb_ldc_views_and_shard_equality():
@@ -288,7 +335,9 @@ def test_spmm_full_size_bert_sampled(wl):
     parts = oracle.compress(A, F16, V=V, M=M)
     for g, e in zip(got, parts):
         assert np.array_equal(g.reshape(e.shape), e)
-    C = venom.spmm(x, to_dev(B, F16))
     cols = np.random.Generator(np.random.PCG64(1)).choice(T, size=64, replace=False)
     C_ref = oracle.spmm(*parts, R, K, F16, V, M, np.ascontiguousarray(B[:, cols]))
-    check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)
+    Bd = to_dev(B, F16)
+    for strat in strategies(K, V, M):
+        C = venom.spmm(x, Bd, strategy=strat)
+        check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)
