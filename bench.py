@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -106,47 +105,50 @@ def aggregate(per_rank_units: float, ws: int, t_max_s: float) -> float:
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples the SM clock and clock-event (throttle) reasons through NVML from a background
+    thread every ~2 ms while the timed region runs (the main thread mostly sleeps in CUDA syncs)."""
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
 
     def __init__(self, index: int):
-        self.proc = None
-        self.index = index
+        import threading
+        self.samples, self.reasons, self.smax = [], set(), None
+        self.err = None
+        self._stop = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as ex:  # pragma: no cover - no NVML on this host
+            self.nv, self.err = None, repr(ex)
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        import time as _t
+        while self.nv is not None and not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, const in self.REASONS:
+                    if mask & getattr(self.nv, const, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            _t.sleep(0.002)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            parts = [s.strip() for s in line.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower() in ("active", "1", "yes"):
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        self.t.join(timeout=2)
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": [self.err or "no samples"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ----------------------------------------------------------------------------- GPU workload
@@ -195,9 +197,13 @@ def run_gpu(args, ws, rank, local):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
 
-    def step(spmm_events=None):
+    def step(spmm_events=None, part_events=None):
+        if part_events is not None:
+            part_events[0].record(stream)
         for L in layers:
             L.compress()
+        if part_events is not None:
+            part_events[1].record(stream)
         for i, L in enumerate(layers):
             if spmm_events is not None:
                 spmm_events[i][0].record(stream)
@@ -205,8 +211,12 @@ def run_gpu(args, ws, rank, local):
             if spmm_events is not None:
                 spmm_events[i][1].record(stream)
         if args.step == "full":
+            if part_events is not None:
+                part_events[2].record(stream)
             for L in layers:
                 L.decompress()
+            if part_events is not None:
+                part_events[3].record(stream)
 
     launches_per_step = len(layers) * (3 if args.step == "full" else 2)
     for _ in range(args.warmup):
@@ -217,19 +227,22 @@ def run_gpu(args, ws, rank, local):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sp_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in layers]
              for _ in range(args.steps)]
+    pt_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     clocks = ClockSampler(device.index if device.index is not None else 0)
     barrier(ws)
     torch.cuda.synchronize(device)
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record(stream)
-        step(sp_ev[k])
+        step(sp_ev[k], pt_ev[k])
         ev[k][1].record(stream)
     torch.cuda.synchronize(device)
     barrier(ws)
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     spmm_ms = [[a.elapsed_time(b) for a, b in row] for row in sp_ev]
+    compress_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in pt_ev)
+    decompress_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in pt_ev) if args.step == "full" else 0.0
     total_s = max_over_ranks(sum(step_ms) / 1e3, ws, device)
     flops_step = sum(L.flops for L in layers)
     value = aggregate(flops_step * args.steps, ws, total_s) / 1e12
@@ -327,6 +340,10 @@ def run_gpu(args, ws, rank, local):
                        "step": ("compress+spmm+decompress per layer" if args.step == "full" else "spmm per layer"),
                        "l2": "flushed (512 MiB write) before every timed step", "parallelism": f"T-split x{ws}"},
             "spmm_only": {"tflops": round(achieved, 3), "ms_per_launch": [round(x, 5) for x in per_launch_ms]},
+            "step_breakdown_ms": {"compress_all_layers": round(compress_ms, 5),
+                                  "spmm_all_layers": round(sum(per_launch_ms), 5),
+                                  "decompress_all_layers": round(decompress_ms, 5),
+                                  "compress_GBps": round(sum(2 * L.w["R"] * L.w["K"] for L in layers) / compress_ms / 1e6, 1)},
             "speedup_vs_cublas": [round(s, 3) for s in speedup],
             "cublas_ms": [round(c, 5) for c in cub],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -364,7 +381,7 @@ def time_oracle(hosts, budget_s: float, kind: str = "oracle"):
     for (w, A, B), parts in zip(hosts, comp):
         oracle.spmm(*parts, w["R"], w["K"], oracle.F16, w["V"], w["M"], np.ascontiguousarray(B[:, :cols]))
     t_cal = time.perf_counter() - t1
-    T = min(h[0]["T"] for h in hosts)
+    T = min(min(h[0]["T"], h[2].shape[1]) for h in hosts)  # columns actually available
     cols2 = int(max(8, min(T, cols * max(1.0, (budget_s - t_comp) / max(t_cal, 1e-3)))))
     cols2 -= cols2 % 8
     t2 = time.perf_counter()

@@ -31,52 +31,92 @@ __device__ __forceinline__ bool bits_non_finite(uint16_t b) {
 // Compression. grid = (ceil(G / gpc), R / V), block = 256 threads.
 // One CTA owns one row-block rb and a chunk of `gpc` consecutive groups (gpc even, so metadata
 // bytes — two groups each — are never shared between CTAs).
-//   phase 1: thread per column: s = Σ_{rows ascending} |a| in fp64 (coalesced row sweeps)
+//   phase 1: column L1 mass over the block's V rows in fp64. Each thread sums VEC adjacent
+//            columns (16-byte loads when VEC = 8) over a contiguous range of rows, ascending.
+//            fp16: |a| are multiples of 2^-24 below 2^16, so fp64 partial sums over row ranges
+//            are exact and their (fixed-order) total is bit-identical to the oracle's sequential
+//            sum; the rows are split over the idle threads. bf16: one range (sequential, same
+//            order as the oracle: exactness is not guaranteed, order is).
 //   phase 2: thread per group: top-4 columns by (s desc, index asc), sorted ascending
 //   phase 3: thread per (row, pair of groups): top-2 of the 4 by (|a| desc, position asc),
 //            raw-bit value copy, nibble packing — one metadata byte and 8 value bytes per thread.
-template <bool kBF16>
+template <bool kBF16, int VEC>
 __global__ void __launch_bounds__(256) vnm_compress_kernel(
     const uint16_t* __restrict__ A, int64_t R, int64_t K, int64_t lda, int V, int M, int64_t G,
     int gpc, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
     uint8_t* __restrict__ column_idx, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  double* s_score = reinterpret_cast<double*>(smem_raw);                       // gpc * M
-  uint8_t* s_sel = smem_raw + sizeof(double) * static_cast<size_t>(gpc) * M;   // gpc * 4
-
   const int64_t rb = blockIdx.y;
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * gpc;
   const int ng = static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
   const int ncols = ng * M;
+  const int wmax = gpc * M;
+  const int ncv = (ncols + VEC - 1) / VEC;                 // column vectors in this chunk
+  const int ncv_max = (wmax + VEC - 1) / VEC;
+  const int nsplit_max = kBF16 ? 1 : (static_cast<int>(blockDim.x) / ncv_max > 0 ? static_cast<int>(blockDim.x) / ncv_max : 1);
+  double* s_part = reinterpret_cast<double*>(smem_raw);                      // nsplit_max × wmax
+  double* s_score = s_part;                                                  // reused: row 0
+  uint8_t* s_sel = smem_raw + sizeof(double) * static_cast<size_t>(nsplit_max) * wmax;  // gpc × 4
   const int64_t k0 = g0 * M;
   const int64_t row0 = rb * V;
   const int64_t meta_row = (G + 1) / 2;
+  const int nsplit = nsplit_max < V ? nsplit_max : V;  // row ranges (fp16 only; smem-sized)
 
-  // ---- phase 1: column L1 mass, fp64, ascending rows (exact for fp16; fixed order for bf16)
+  // ---- phase 1: column L1 mass, fp64, ascending rows within each range
   bool bad = false;
-  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-    const uint16_t* col = A + row0 * lda + k0 + c;
-    double s = 0.0;
-    int i = 0;
-    for (; i + 8 <= V; i += 8) {
-      uint16_t b[8];
+  for (int t = threadIdx.x; t < ncv * nsplit; t += blockDim.x) {
+    const int cv = t % ncv, sp = t / ncv;
+    const int rbeg = static_cast<int>((static_cast<int64_t>(V) * sp) / nsplit);
+    const int rend = static_cast<int>((static_cast<int64_t>(V) * (sp + 1)) / nsplit);
+    const int c0 = cv * VEC;
+    const uint16_t* col = A + row0 * lda + k0 + c0;
+    double acc[VEC];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) b[u] = __ldg(col + static_cast<int64_t>(i + u) * lda);
+    for (int u = 0; u < VEC; ++u) acc[u] = 0.0;
+    const bool full = (VEC == 1) || (c0 + VEC <= ncols);
+    int i = rbeg;
+    if (VEC == 8 && full) {
+      for (; i + 4 <= rend; i += 4) {
+        uint4 w[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        bad |= bits_non_finite<kBF16>(b[u]);
-        s = __dadd_rn(s, static_cast<double>(fabsf(bits_to_float<kBF16>(b[u]))));
+        for (int q = 0; q < 4; ++q) w[q] = __ldg(reinterpret_cast<const uint4*>(col + static_cast<int64_t>(i + q) * lda));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t ww[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) {
+            const uint16_t b = static_cast<uint16_t>((ww[u >> 1] >> (16 * (u & 1))) & 0xFFFFu);
+            bad |= bits_non_finite<kBF16>(b);
+            acc[u] = __dadd_rn(acc[u], static_cast<double>(fabsf(bits_to_float<kBF16>(b))));
+          }
+        }
       }
     }
-    for (; i < V; ++i) {
-      uint16_t b = __ldg(col + static_cast<int64_t>(i) * lda);
-      bad |= bits_non_finite<kBF16>(b);
-      s = __dadd_rn(s, static_cast<double>(fabsf(bits_to_float<kBF16>(b))));
+    for (; i < rend; ++i) {
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        if (c0 + u < ncols) {
+          const uint16_t b = __ldg(col + static_cast<int64_t>(i) * lda + u);
+          bad |= bits_non_finite<kBF16>(b);
+          acc[u] = __dadd_rn(acc[u], static_cast<double>(fabsf(bits_to_float<kBF16>(b))));
+        }
+      }
     }
-    s_score[c] = s;
+#pragma unroll
+    for (int u = 0; u < VEC; ++u)
+      if (c0 + u < ncols) s_part[sp * wmax + c0 + u] = acc[u];
   }
   if (bad && status != nullptr) atomicMax(status, kStatusNonFinite);
   __syncthreads();
+  if (nsplit > 1) {
+    // fixed-order total of the exact fp16 partial sums
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+      double sum = s_part[c];
+      for (int sp = 1; sp < nsplit; ++sp) sum = __dadd_rn(sum, s_part[sp * wmax + c]);
+      s_part[c] = sum;  // s_score aliases row 0: each thread only touches its own column
+    }
+    __syncthreads();
+  }
 
   // ---- phase 2: the four most significant columns of each block
   for (int q = threadIdx.x; q < ng; q += blockDim.x) {
@@ -168,62 +208,69 @@ __global__ void __launch_bounds__(256) vnm_compress_kernel(
   }
 }
 
-// Decompression: thread per (row, 8 consecutive output elements). Output +0.0 except the kept
-// positions. Validates metadata when `status` is non-null.
+// Decompression: grid (column chunks, rows); thread per (row, kVec consecutive output elements).
+// Output +0.0 except the kept positions. Validates metadata when `status` is non-null. 32-bit
+// index arithmetic inside a row (K < 2^31), group/position advanced incrementally.
 template <int kVec>
 __global__ void __launch_bounds__(256) vnm_decompress_kernel(
     const uint16_t* __restrict__ values, const uint8_t* __restrict__ metadata,
     const uint8_t* __restrict__ column_idx, int64_t R, int64_t K, int V, int M, int64_t G,
     uint16_t* __restrict__ out, int64_t lda, int32_t* __restrict__ status) {
   const int64_t meta_row = (G + 1) / 2;
-  const int64_t chunks = (K + kVec - 1) / kVec;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= R * chunks) return;
-  const int64_t row = idx / chunks;
-  const int64_t k0 = (idx - row * chunks) * kVec;
-  const int64_t rb = row / V;
-  uint16_t o[kVec];
-  int64_t cur_g = -1;
-  int c0 = 0, c1 = 0;
-  uint16_t v0 = 0, v1 = 0;
+  const int kk = static_cast<int>(K);
+  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * kVec;
+  if (k0 >= kk) return;
   bool bad = false;
+  for (int64_t row = blockIdx.y; row < R; row += gridDim.y) {
+    const int64_t rb = row / V;
+    const uint32_t* cw_row = reinterpret_cast<const uint32_t*>(column_idx) + rb * G;
+    const uint32_t* v_row = reinterpret_cast<const uint32_t*>(values) + row * G;
+    const uint8_t* m_row = metadata + row * meta_row;
+    int g = k0 / M;
+    int j = k0 - g * M;
+    uint16_t o[kVec];
+    int c0 = -1, c1 = -1;
+    uint16_t v0 = 0, v1 = 0;
+    int cur_g = -1;
 #pragma unroll
-  for (int u = 0; u < kVec; ++u) {
-    const int64_t k = k0 + u;
-    o[u] = 0;
-    if (k >= K) continue;
-    const int64_t g = k / M;
-    if (g != cur_g) {
-      cur_g = g;
-      const uint32_t cw = __ldg(reinterpret_cast<const uint32_t*>(column_idx) + rb * G + g);
-      const int c[4] = {int(cw & 0xFF), int((cw >> 8) & 0xFF), int((cw >> 16) & 0xFF),
-                        int(cw >> 24)};
-      const uint32_t nib = (__ldg(metadata + row * meta_row + g / 2) >> (4 * (g & 1))) & 0xF;
-      const int p0 = nib & 3, p1 = nib >> 2;
-      bad |= !(c[0] < c[1] && c[1] < c[2] && c[2] < c[3] && c[3] < M) || !(p0 < p1);
-      c0 = c[p0];
-      c1 = c[p1];
-      const uint32_t vv = __ldg(reinterpret_cast<const uint32_t*>(values) + row * G + g);
-      v0 = static_cast<uint16_t>(vv & 0xFFFF);
-      v1 = static_cast<uint16_t>(vv >> 16);
+    for (int u = 0; u < kVec; ++u) {
+      o[u] = 0;
+      if (k0 + u < kk) {
+        if (g != cur_g) {
+          cur_g = g;
+          const uint32_t cw = __ldg(cw_row + g);
+          const uint32_t nib = (__ldg(m_row + (g >> 1)) >> (4 * (g & 1))) & 0xFu;
+          const uint32_t p0 = nib & 3u, p1 = nib >> 2;
+          const uint32_t ca = cw & 0xFFu, cb = (cw >> 8) & 0xFFu, cc = (cw >> 16) & 0xFFu, cd = cw >> 24;
+          bad |= !(ca < cb && cb < cc && cc < cd && cd < static_cast<uint32_t>(M)) || !(p0 < p1);
+          c0 = static_cast<int>((cw >> (8 * p0)) & 0xFFu);
+          c1 = static_cast<int>((cw >> (8 * p1)) & 0xFFu);
+          const uint32_t vv = __ldg(v_row + g);
+          v0 = static_cast<uint16_t>(vv & 0xFFFFu);
+          v1 = static_cast<uint16_t>(vv >> 16);
+        }
+        o[u] = (j == c0) ? v0 : ((j == c1) ? v1 : static_cast<uint16_t>(0));
+      }
+      if (++j == M) {
+        j = 0;
+        ++g;
+      }
     }
-    const int j = static_cast<int>(k - g * M);
-    o[u] = (j == c0) ? v0 : ((j == c1) ? v1 : static_cast<uint16_t>(0));
+    uint16_t* dst = out + row * lda + k0;
+    if (kVec == 8 && k0 + 8 <= kk) {
+      uint4 w;
+      w.x = o[0] | (uint32_t(o[1]) << 16);
+      w.y = o[2] | (uint32_t(o[3]) << 16);
+      w.z = o[4] | (uint32_t(o[5]) << 16);
+      w.w = o[6] | (uint32_t(o[7]) << 16);
+      *reinterpret_cast<uint4*>(dst) = w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (k0 + u < kk) dst[u] = o[u];
+    }
   }
   if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
-  uint16_t* dst = out + row * lda + k0;
-  if (kVec == 8 && k0 + 8 <= K) {
-    uint4 w;
-    w.x = o[0] | (uint32_t(o[1]) << 16);
-    w.y = o[2] | (uint32_t(o[3]) << 16);
-    w.z = o[4] | (uint32_t(o[5]) << 16);
-    w.w = o[6] | (uint32_t(o[7]) << 16);
-    *reinterpret_cast<uint4*>(dst) = w;
-  } else {
-#pragma unroll
-    for (int u = 0; u < kVec; ++u)
-      if (k0 + u < K) dst[u] = o[u];
-  }
 }
 
 }  // namespace venom

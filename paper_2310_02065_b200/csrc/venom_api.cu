@@ -198,22 +198,30 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
   if (!aligned(values, 8) || !aligned(column_idx, 4) || !aligned(A, 2)) return VENOM_ERR_INVALID_ARGUMENT;
   if ((st = check_arch()) != VENOM_OK) return st;
   const int64_t G = K / f.m;
-  int gpc = 512 / f.m;
+  // ~256 columns per CTA (whole, even number of groups), so that R/V × K/256 CTAs stream A
+  int gpc = 256 / f.m;
   gpc -= gpc & 1;
   if (gpc < 2) gpc = 2;
   if (gpc > G + (G & 1)) gpc = static_cast<int>(G + (G & 1));
+  const bool vec = aligned(A, 16) && (lda % 8 == 0) && ((static_cast<int64_t>(gpc) * f.m) % 8 == 0);
   const dim3 grid(static_cast<unsigned>((G + gpc - 1) / gpc), static_cast<unsigned>(R / f.v));
   if (grid.y > 65535u) return VENOM_ERR_INVALID_ARGUMENT;
-  const size_t smem = sizeof(double) * static_cast<size_t>(gpc) * f.m + 4 * static_cast<size_t>(gpc);
+  const int wmax = gpc * f.m;
+  const int vecw = vec ? 8 : 1;
+  const int ncv_max = (wmax + vecw - 1) / vecw;
+  const int nsplit_max = (dt == VENOM_BF16) ? 1 : (256 / ncv_max > 0 ? 256 / ncv_max : 1);
+  const size_t smem = sizeof(double) * static_cast<size_t>(nsplit_max) * wmax + 4 * static_cast<size_t>(gpc);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dt == VENOM_BF16)
-    venom::vnm_compress_kernel<true><<<grid, 256, smem, s>>>(
-        static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values),
-        metadata, column_idx, dev_status);
-  else
-    venom::vnm_compress_kernel<false><<<grid, 256, smem, s>>>(
-        static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values),
-        metadata, column_idx, dev_status);
+#define VENOM_COMPRESS(BF, VW)                                                                     \
+  venom::vnm_compress_kernel<BF, VW><<<grid, 256, smem, s>>>(                                      \
+      static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values), \
+      metadata, column_idx, dev_status)
+  if (dt == VENOM_BF16) {
+    if (vec) VENOM_COMPRESS(true, 8); else VENOM_COMPRESS(true, 1);
+  } else {
+    if (vec) VENOM_COMPRESS(false, 8); else VENOM_COMPRESS(false, 1);
+  }
+#undef VENOM_COMPRESS
   return launch_status();
 }
 
@@ -233,15 +241,16 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool vec = aligned(A_out, 16) && (lda % 8 == 0);
   const int kv = vec ? 8 : 1;
-  const int64_t work = R * ((K + kv - 1) / kv);
-  const int64_t blocks = (work + 255) / 256;
-  if (blocks > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  const int64_t chunks = (K + kv - 1) / kv;
+  if (K > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  const dim3 grid(static_cast<unsigned>((chunks + 255) / 256),
+                  static_cast<unsigned>(R < 65535 ? R : 65535));
   if (vec)
-    venom::vnm_decompress_kernel<8><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+    venom::vnm_decompress_kernel<8><<<grid, 256, 0, s>>>(
         static_cast<const uint16_t*>(values), metadata, column_idx, R, K, f.v, f.m, G,
         static_cast<uint16_t*>(A_out), lda, dev_status);
   else
-    venom::vnm_decompress_kernel<1><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+    venom::vnm_decompress_kernel<1><<<grid, 256, 0, s>>>(
         static_cast<const uint16_t*>(values), metadata, column_idx, R, K, f.v, f.m, G,
         static_cast<uint16_t*>(A_out), lda, dev_status);
   return launch_status();
