@@ -131,6 +131,8 @@ typedef struct {
   int32_t stages;
   int32_t max_ctas;
   int32_t strategy;
+  int32_t cta_pair;  /* dense-K only: 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2,
+                        256-row tiles, B split between the pair's shared memories); 0 = default 2 */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

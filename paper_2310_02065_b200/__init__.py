@@ -45,7 +45,7 @@ class _Format(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
-                ("strategy", ctypes.c_int32)]
+                ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -184,7 +184,7 @@ def decompress(x: VNMTensor, out: Optional[torch.Tensor] = None, status: Optiona
 
 def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
-         max_ctas: int = 0, strategy: int = STRATEGY_AUTO) -> torch.Tensor:
+         max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T]."""
     assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[0] == x.K
@@ -195,7 +195,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     assert out.stride(1) == 1 and out.shape == (x.R, T)
     if bias is not None:
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
-    opts = _Opts(tile_t, stages, max_ctas, strategy)
+    opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
                              ctypes.c_void_p(x.column_idx.data_ptr()), x.R, x.K, x.fmt(),
                              ctypes.c_void_p(B.data_ptr()), T, B.stride(0),

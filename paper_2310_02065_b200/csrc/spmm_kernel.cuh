@@ -124,23 +124,30 @@ __device__ __forceinline__ void load_meta_stage(const SpmmParams& p, int64_t row
 
 // Persistent static schedule: CTA b runs tiles b, b + grid, b + 2·grid, ... in T-band order (all
 // row tiles of one column band first, so concurrently running CTAs share the B column slab in L2).
+// With CTA pairs (CG = 2) the unit of scheduling is the cluster: pair b runs tiles b, b + pairs...
+template <int CG = 1>
 __device__ __forceinline__ void tile_coords(const SpmmParams& p, int tl, int& m_tile, int& n_tile) {
-  const int t = static_cast<int>(blockIdx.x) + tl * static_cast<int>(gridDim.x);
+  const int t = static_cast<int>(blockIdx.x) / CG + tl * (static_cast<int>(gridDim.x) / CG);
   n_tile = t / p.m_tiles;
   m_tile = t - n_tile * p.m_tiles;
+}
+template <int CG = 1>
+__device__ __forceinline__ int my_tile_count(const SpmmParams& p) {
+  const int gid = static_cast<int>(blockIdx.x) / CG, ng = static_cast<int>(gridDim.x) / CG;
+  return gid < p.num_tiles ? (p.num_tiles - gid + ng - 1) / ng : 0;
 }
 
 // MMA issuer (one elected lane of one warp): per k-stage, copy the stage's metadata SMEM->TMEM
 // (tcgen05.cp, 128 lanes × 4 words) and issue 4 sparse MMAs (K = 32 each) per V-block.
 // Stage layout (both kernels): [A 16 KB K-major SW128][NB × B' (BN/64 chunks × 16 KB, MN-major
 // SW128)][metadata 2 KB: lane L at 16·L].
-template <class Cfg, bool kBF16>
+template <class Cfg, bool kBF16, int CG = 1>
 __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                          uint32_t smem0, uint32_t full0, uint32_t empty0,
                                          uint32_t accf0, uint32_t acce0, int lane) {
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
-  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128, BN);
+  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128 * CG, BN);
   for (int tl = 0; tl < my_tiles; ++tl) {
     const int ab = tl % Cfg::ACC_BUFS;
     const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
@@ -157,7 +164,9 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
         const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
         const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * (it & 1);
         // metadata: 128 rows × 16 B, core matrices of 8 rows contiguous (SBO = 128 B)
-        tc_cp_128x128b(e_tmem, smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0));
+        const uint64_t edesc = smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0);
+        if constexpr (CG == 2) tc_cp_128x128b_2sm(e_tmem, edesc);
+        else tc_cp_128x128b(e_tmem, edesc);
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           const uint32_t e_addr = e_tmem + kb;
@@ -170,12 +179,21 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
             // K advance 32 rows = 4096 B per MMA
             const uint64_t bdesc =
                 smem_desc(sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + kb * 4096, Cfg::B_CHUNK, 1024, 2);
-            tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
-                          (ks | kb) != 0 ? 1u : 0u);
+            if constexpr (CG == 2)
+              tc_mma_sp_f16_2sm(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
+                                (ks | kb) != 0 ? 1u : 0u);
+            else
+              tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
+                            (ks | kb) != 0 ? 1u : 0u);
           }
         }
-        tc_commit(empty0 + 8 * stage);
-        if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
+        if constexpr (CG == 2) {
+          tc_commit_2sm_mc(empty0 + 8 * stage, 0x3);
+          if (ks == p.num_ks - 1) tc_commit_2sm_mc(accf0 + 8 * ab, 0x3);
+        } else {
+          tc_commit(empty0 + 8 * stage);
+          if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
+        }
         VENOM_TRACE_EVENT(2, it);
       }
       __syncwarp();
@@ -185,20 +203,21 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 
 // Epilogue (4 warps, one TMEM lane quarter each): TMEM -> +bias (fp32) -> RNE to fp16/bf16 ->
 // 16-byte global stores; releases the accumulator buffer to the MMA warp.
-template <class Cfg, bool kBF16>
+template <class Cfg, bool kBF16, int CG = 1>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane) {
   using namespace ptx;
   constexpr int NB = Cfg::NB, BN = Cfg::BN;
   const int q = warp & 3;  // TMEM lane quarter this warp may access
-  const int r_local = 32 * q + lane;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const int r_local = 128 * static_cast<int>(rank) + 32 * q + lane;  // row within the (pair) tile
   for (int tl = 0; tl < my_tiles; ++tl) {
     int m_tile, n_tile;
-    tile_coords(p, tl, m_tile, n_tile);
+    tile_coords<CG>(p, tl, m_tile, n_tile);
     const int ab = tl % Cfg::ACC_BUFS;
     mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
     tc_fence_after();
-    const int64_t row = static_cast<int64_t>(m_tile) * 128 + r_local;
+    const int64_t row = static_cast<int64_t>(m_tile) * (128 * CG) + r_local;
     const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
     const float bv = (p.bias != nullptr && row < p.R)
                          ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
@@ -230,7 +249,10 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(acce0 + 8 * ab);
+    if (lane == 0) {
+      if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(acce0 + 8 * ab, 0));  // pair leader
+      else mbar_arrive(acce0 + 8 * ab);
+    }
   }
 }
 

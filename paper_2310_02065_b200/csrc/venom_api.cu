@@ -110,20 +110,40 @@ venom_status_t run_densek(const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid < 1) return VENOM_OK;
-  kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tb, tv, p);
+  if constexpr (Cfg::CG == 1) {
+    kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tb, tv, p);
+  } else {
+    grid -= grid % Cfg::CG;  // whole CTA pairs
+    if (grid < Cfg::CG) grid = Cfg::CG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cfg::NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Cfg::CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, tb, tv, p) != cudaSuccess) return VENOM_ERR_CUDA;
+  }
   return launch_status();
 }
 
-template <int BN, int ST>
+template <int BN, int ST, int CG = 1>
 venom_status_t run_densek_m(int M, bool bf16, const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p,
                             int max_ctas, cudaStream_t s) {
+  p.m_tiles = static_cast<int>((p.R + 128 * CG - 1) / (128 * CG));
+  p.num_tiles = p.m_tiles * p.n_tiles;
 #define VENOM_DK(MM)                                                                      \
   case MM:                                                                                \
-    return bf16 ? run_densek<DenseKCfg<BN, ST, MM>, true>(tb, enc, p, max_ctas, s)        \
-                : run_densek<DenseKCfg<BN, ST, MM>, false>(tb, enc, p, max_ctas, s);
+    return bf16 ? run_densek<DenseKCfg<BN, ST, MM, CG>, true>(tb, enc, p, max_ctas, s)    \
+                : run_densek<DenseKCfg<BN, ST, MM, CG>, false>(tb, enc, p, max_ctas, s);
   switch (M) {
     VENOM_DK(4) VENOM_DK(8) VENOM_DK(16) VENOM_DK(32)
   }
@@ -350,8 +370,14 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     p.num_ks = static_cast<int>((K + 127) / 128);
     if (tile_t == 0) tile_t = 256;
     set_tiles(tile_t);
-    if (tile_t == 256) return run_densek_m<256, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
-    if (tile_t == 128) return run_densek_m<128, 3>(f.m, bf16, tb, enc, p, max_ctas, s);
+    const int pair = opts && opts->cta_pair ? opts->cta_pair : 2;
+    if (pair == 2) {
+      if (tile_t == 256) return run_densek_m<256, 4, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
+      if (tile_t == 128) return run_densek_m<128, 6, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
+    } else {
+      if (tile_t == 256) return run_densek_m<256, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
+      if (tile_t == 128) return run_densek_m<128, 4>(f.m, bf16, tb, enc, p, max_ctas, s);
+    }
     return VENOM_ERR_INVALID_ARGUMENT;
   }
 

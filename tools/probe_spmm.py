@@ -11,7 +11,7 @@ from tests.helpers import bits_to_f64, f64_to_bits
 def dev(bits):
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.float16).cuda()
 
-def run(R, K, T, V, M, Akind, Bkind, tile_t=0, strategy=0):
+def run(R, K, T, V, M, Akind, Bkind, tile_t=0, strategy=0, pair=0):
     if Akind == "ones":
         A = f64_to_bits(np.ones((R, K)), 0)
     elif Akind == "rowid":
@@ -28,11 +28,11 @@ def run(R, K, T, V, M, Akind, Bkind, tile_t=0, strategy=0):
     vals, meta, cidx = oracle.compress(A, 0, V=V, M=M)
     ref = oracle.spmm(vals, meta, cidx, R, K, 0, V, M, B)
     x = venom.VNMTensor(dev(vals), torch.from_numpy(meta).cuda(), torch.from_numpy(cidx).cuda(), R, K, V, M)
-    C = venom.spmm(x, dev(B), tile_t=tile_t, strategy=strategy)
+    C = venom.spmm(x, dev(B), tile_t=tile_t, strategy=strategy, cta_pair=pair)
     torch.cuda.synchronize()
     got = C.double().cpu().numpy()
     bad = ~np.isclose(got, ref, rtol=2e-2, atol=1e-2)
-    print(f"== R{R} K{K} T{T} V{V} M{M} A={Akind} B={Bkind} tile={tile_t} strat={strategy}: bad {bad.sum()}/{bad.size}")
+    print(f"== R{R} K{K} T{T} V{V} M{M} A={Akind} B={Bkind} tile={tile_t} strat={strategy} pair={pair}: bad {bad.sum()}/{bad.size}")
     if bad.any():
         rows = np.nonzero(bad.any(1))[0]
         cols = np.nonzero(bad.any(0))[0]
@@ -49,6 +49,15 @@ def run(R, K, T, V, M, Akind, Bkind, tile_t=0, strategy=0):
 if __name__ == "__main__":
     torch.cuda.init()
     import sys as _s
+    if len(_s.argv) > 1 and _s.argv[1] == "pair":
+        for c in [(256, 256, 256, 128, 8, "gauss", "eye", 256, 2, 2), (256, 1024, 512, 128, 8, "gauss", "gauss", 256, 2, 2),
+                  (128, 1024, 512, 128, 8, "gauss", "gauss", 256, 2, 2), (384, 1024, 512, 64, 4, "gauss", "gauss", 256, 2, 2),
+                  (512, 2048, 512, 64, 16, "gauss", "gauss", 128, 2, 2), (512, 1024, 1024, 128, 8, "gauss", "eye", 256, 2, 2)]:
+            try:
+                run(*c)
+            except Exception as e:
+                print("EXC", c, repr(e))
+        _s.exit(0)
     if len(_s.argv) > 1 and _s.argv[1] == "densek":
         for c in [(128, 1024, 512, 128, 4, "gauss", "gauss", 256, 2), (128, 1024, 512, 128, 4, "gauss", "gauss", 128, 2),
                   (128, 1024, 512, 128, 8, "gauss", "gauss", 256, 2), (128, 1024, 1024, 128, 4, "gauss", "eye", 256, 2), (128, 1024, 1024, 128, 16, "gauss", "eye", 256, 2),

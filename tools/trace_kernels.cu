@@ -15,6 +15,7 @@ int main(int argc, char** argv) {
              T = argc > 3 ? atol(argv[3]) : 4096;
   const int V = argc > 4 ? atoi(argv[4]) : 64, M = argc > 5 ? atoi(argv[5]) : 8;
   const int strat = argc > 6 ? atoi(argv[6]) : 2, tile = argc > 7 ? atoi(argv[7]) : 0;
+  const int pair = argc > 8 ? atoi(argv[8]) : 0;
   const long G = K / M;
   uint16_t *vals, *B, *C;
   uint8_t *meta, *cidx;
@@ -32,7 +33,7 @@ int main(int argc, char** argv) {
   const size_t ntr = 2 * 16 * 256;
   cudaMalloc(&tr, ntr * 8);
   cudaMemcpyToSymbol(g_venom_trace, &tr, sizeof(tr));
-  venom_spmm_opts_t o{tile, 0, 0, strat};
+  venom_spmm_opts_t o{tile, 0, 0, strat, pair};
   venom_format_t f{V, 2, M};
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemset(tr, 0, ntr * 8);
