@@ -104,7 +104,7 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  * Requirements (else VENOM_ERR_UNSUPPORTED_PATTERN / INVALID_ARGUMENT):
  *   V | R; M in [4,256], M | K; T % 8 == 0, ldb % 8 == 0, ldc % 8 == 0, ldb >= T, ldc >= T;
  *   values/B/C 16-byte aligned; and at least one strategy applies:
- *     gather : V in {32, 64} or V % 128 == 0, and G = K/M with G % 4 == 0
+ *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0
  *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
  *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
  * Metadata validity is NOT checked here (use venom_decompress with dev_status to validate);

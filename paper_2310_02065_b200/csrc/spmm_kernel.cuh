@@ -48,36 +48,40 @@ struct SpmmParams {
   int dbg;  // debug/ablation flags (0 in production)
 };
 
-template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8>
+template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8, int CG_ = 1>
 struct SpmmCfg {
   static constexpr int NB = NB_;              // V-blocks per 128-row tile
+  static constexpr int CG = CG_;              // 2: CTA pair (cta_group::2, 256-row tiles): needs
+                                              // one column_idx per pair tile (V % 256 == 0 or M == 4)
   static constexpr int BN = BN_;              // output columns per tile (MMA N)
+  static constexpr int BNH = BN / CG_;        // B' columns staged by one CTA
   static constexpr int STAGES = STAGES_;
   static constexpr int P = PRODUCERS_;        // gather-issuing warps (TMA issue is per-warp serial)
-  static constexpr int BM = 128;              // MMA M
+  static constexpr int BM = 128;              // rows per CTA
   static constexpr int KG = 32;               // groups per k-stage: K' = 128, 4 MMAs of K = 32
   static constexpr int A_BYTES = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
   static constexpr int B_CHUNK = 128 * 128;   // 128 K'-rows × 64 columns × 2 B (SW128, MN-major)
-  static constexpr int B_BYTES = (BN / 64) * B_CHUNK;
-  static constexpr int E_BYTES = 128 * 16;    // 128 lanes × 4 metadata words
-  static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES + E_BYTES;
-  static constexpr int TX_BYTES = A_BYTES + NB * B_BYTES;
+  static constexpr int B_BYTES = (BNH / 64) * B_CHUNK;
+  static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES;
+  static constexpr int TX_BYTES = A_BYTES + NB * B_BYTES;  // per CTA
   static constexpr int ACC_COLS = NB * BN;
-  static constexpr int E_COLS = 8;            // two 4-column metadata regions
-  static constexpr int ACC_BUFS = (2 * ACC_COLS + E_COLS <= 512) ? 2 : 1;
-  static constexpr int E_COL = 512 - E_COLS;
-  static constexpr int NCH = BN / 64;         // 64-column chunks of B' per block
+  // TMEM: accumulators, then 4 metadata columns per stage (written by tcgen05.st)
+  static constexpr int ACC_BUFS = (2 * ACC_COLS + 4 * STAGES_ <= 512) ? 2 : 1;
+  static constexpr int E_COL = ACC_BUFS * ACC_COLS;
+  static constexpr int NCH = BNH / 64;        // 64-column chunks of B' per block
   static constexpr int NOPS = NB * NCH * 32;  // gather4 ops per stage (one per group × chunk × block)
   static constexpr int OPS_PER_WARP = NOPS / P;
   static constexpr int LANE_OPS = (OPS_PER_WARP + 31) / 32;
-  // warp roles: [0,P) producers, P MMA, P+1..P+4 epilogue, P+5..P+8 metadata
+  // warp roles: [0,P) producers, P MMA, P+1..P+4 epilogue, P+5..P+8 metadata; epilogue and
+  // metadata warps address TMEM lane quarter (warp % 4)
   static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 5;
   static constexpr int NUM_THREADS = 32 * (P + 9);
   static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
+  static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
   static constexpr int BAR_BYTES = 256;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
-  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN");
-  static_assert(ACC_BUFS * ACC_COLS + E_COLS <= 512, "TMEM budget");
+  static_assert(BNH % 64 == 0 && BN <= 256, "BN");
+  static_assert(E_COL + 4 * STAGES_ <= 512, "TMEM budget");
   static_assert(STAGE_BYTES % 1024 == 0, "stage alignment");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
@@ -137,10 +141,9 @@ __device__ __forceinline__ int my_tile_count(const SpmmParams& p) {
   return gid < p.num_tiles ? (p.num_tiles - gid + ng - 1) / ng : 0;
 }
 
-// MMA issuer (one elected lane of one warp): per k-stage, copy the stage's metadata SMEM->TMEM
-// (tcgen05.cp, 128 lanes × 4 words) and issue 4 sparse MMAs (K = 32 each) per V-block.
-// Stage layout (both kernels): [A 16 KB K-major SW128][NB × B' (BN/64 chunks × 16 KB, MN-major
-// SW128)][metadata 2 KB: lane L at 16·L].
+// MMA issuer (one elected lane of the pair leader): per k-stage, 4 sparse MMAs (K = 32) per
+// V-block. Stage layout: [A 16 KB K-major SW128][NB × B' (BNH/64 chunks × 16 KB, MN-major SW128)];
+// the stage's metadata sits in TMEM columns E_COL + 4·stage (written by the metadata warps).
 template <class Cfg, bool kBF16, int CG = 1>
 __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                          uint32_t smem0, uint32_t full0, uint32_t empty0,
@@ -162,11 +165,7 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
       if (lane == 0) VENOM_TRACE_EVENT(1, it);
       if (lane == 0) {
         const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
-        const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * (it & 1);
-        // metadata: 128 rows × 16 B, core matrices of 8 rows contiguous (SBO = 128 B)
-        const uint64_t edesc = smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0);
-        if constexpr (CG == 2) tc_cp_128x128b_2sm(e_tmem, edesc);
-        else tc_cp_128x128b(e_tmem, edesc);
+        const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * stage;
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           const uint32_t e_addr = e_tmem + kb;
@@ -261,7 +260,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b, const SpmmParams p) {
   using namespace ptx;
-  constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
+  constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN, CG = Cfg::CG;
 
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
@@ -277,44 +276,48 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;  // position in the CTA pair
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full0 + 8 * s, 1 + 4);  // producer expect_tx + 4 metadata warps
-      mbar_init(empty0 + 8 * s, 1);     // MMA commit
+      mbar_init(full0 + 8 * s, 1 + 4 * CG);  // leader's expect_tx + metadata warps of the pair
+      mbar_init(empty0 + 8 * s, 1);          // (multicast) MMA commit
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);      // MMA commit
-      mbar_init(acce0 + 8 * b, 4);      // 4 epilogue warps
+      mbar_init(accf0 + 8 * b, 1);           // (multicast) MMA commit
+      mbar_init(acce0 + 8 * b, 4 * CG);      // epilogue warps of the pair
     }
     fence_mbar_init();
     prefetch_tmap(&tm_values);
     prefetch_tmap(&tm_b);
   }
-  if (warp == Cfg::W_MMA) tmem_alloc<512>(smem_u32(tmem_base_slot));
+  if (warp == Cfg::W_MMA) {
+    if constexpr (CG == 2) tmem_alloc_2sm<512>(smem_u32(tmem_base_slot));
+    else tmem_alloc<512>(smem_u32(tmem_base_slot));
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
-  const int my_tiles =
-      (static_cast<int>(blockIdx.x) < p.num_tiles)
-          ? (p.num_tiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
-                static_cast<int>(gridDim.x)
-          : 0;
+  const int my_tiles = my_tile_count<CG>(p);
   const int total = my_tiles * p.num_ks;  // k-stage iterations this CTA runs
   const int nrb = static_cast<int>(p.R / p.V);
+  const int row_off = 128 * static_cast<int>(rank);
+  const bool contiguous = (p.M == 4);  // column_idx ≡ {0,1,2,3}: B' is a plain K-slice of B
 
-  auto tile_of = [&](int tl, int& m_tile, int& n_tile) { tile_coords(p, tl, m_tile, n_tile); };
+  auto tile_of = [&](int tl, int& m_tile, int& n_tile) { tile_coords<CG>(p, tl, m_tile, n_tile); };
   auto block_of = [&](int m_tile, int b) -> int {
-    const int rb = (NB == 1) ? (m_tile * 128) / p.V : m_tile * NB + b;
+    const int rb = (NB == 1) ? (m_tile * 128 * CG + row_off) / p.V : m_tile * NB + b;
     return rb < nrb ? rb : nrb - 1;  // padding block of a ragged last tile: any valid block
   };
 
   if (warp < Cfg::P) {
     // ======================= producers: values tile + gathered B' rows =======================
     // Stage ops are (block b, chunk c, group q); warp w issues ops [w·OPS_PER_WARP, ...), one per
-    // lane: TMA issue is serial within a warp, so the gathers are spread over P warps.
+    // lane: TMA issue is serial within a warp, so the gathers are spread over P warps. With a CTA
+    // pair every TMA signals the leader's barrier (cta_group::2 forms).
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
     uint32_t cw[kPrefetch][Cfg::LANE_OPS];
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
       return true;
     };
     auto fetch = [&](int it, uint32_t (&w)[Cfg::LANE_OPS]) {
-      if (it >= total) return;
+      if (it >= total || contiguous) return;
       int m_tile, n_tile;
       tile_of(it / p.num_ks, m_tile, n_tile);
 #pragma unroll
@@ -356,47 +359,73 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           const int ks = it % p.num_ks;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
+          const uint32_t fbar = (CG == 2) ? mapa_shared(full0 + 8 * stage, 0) : full0 + 8 * stage;
+          const int col0 = n_tile * BN + static_cast<int>(rank) * Cfg::BNH;
+          const int arow = m_tile * 128 * CG + row_off;
           if (warp == 0 && lane == 0) {
-            mbar_arrive_expect_tx(full0 + 8 * stage, Cfg::TX_BYTES);
-            tma_load_2d(sbase, &tm_values, full0 + 8 * stage, ks * 64, m_tile * 128, pol_a);
+            VENOM_TRACE_EVENT(0, it);
+            if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, CG * Cfg::TX_BYTES);
+            if constexpr (CG == 2) tma_load_2d_2sm(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+            else tma_load_2d(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
           }
-          const int col0 = n_tile * BN;
+          if (contiguous && lane == 0) {
+            // M = 4: the 4 "selected" rows of every group are the group itself — plain tile boxes,
+            // one per 64-column chunk, issued by different warps (TMA issue is per-warp serial)
 #pragma unroll
-          for (int j = 0; j < Cfg::LANE_OPS; ++j) {
-            int b, c, q;
-            if (!op_of(j, b, c, q)) continue;
-            const int gg = ks * Cfg::KG + q;
-            const uint32_t w = cw[jj][j];
-            int r[4];
+            for (int b = 0; b < NB; ++b)
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-              r[t] = (gg < p.G) ? gg * p.M + static_cast<int>((w >> (8 * t)) & 0xFF)
-                                : static_cast<int>(p.K);  // past the last row: zero fill
-            const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK + q * 512;
-            tma_gather4(bdst, &tm_b, full0 + 8 * stage, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
+              for (int c = 0; c < Cfg::NCH; ++c) {
+                if ((1 + b * Cfg::NCH + c) % Cfg::P != warp) continue;
+                const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK;
+                if constexpr (CG == 2) tma_load_2d_2sm(bdst, &tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
+                else tma_load_2d(bdst, &tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
+              }
           }
+          if (!contiguous) {
+#pragma unroll
+            for (int j = 0; j < Cfg::LANE_OPS; ++j) {
+              int b, c, q;
+              if (!op_of(j, b, c, q)) continue;
+              const int gg = ks * Cfg::KG + q;
+              const uint32_t w = cw[jj][j];
+              int r[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                r[t] = (gg < p.G) ? gg * p.M + static_cast<int>((w >> (8 * t)) & 0xFF)
+                                  : static_cast<int>(p.K);  // past the last row: zero fill
+              const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK + q * 512;
+              if constexpr (CG == 2)
+                tma_gather4_2sm(bdst, &tm_b, fbar, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
+              else
+                tma_gather4(bdst, &tm_b, fbar, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
+            }
+          }
+          __syncwarp();
           fetch(it + kPrefetch, cw[jj]);
         }
       }
     }
   } else if (warp == Cfg::W_MMA) {
-    mma_role<Cfg, kBF16>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
+    if (rank == 0) mma_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 4) {
-    epilogue_role<Cfg, kBF16>(p, my_tiles, tmem_base, accf0, acce0, warp, lane);
+    epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane);
   } else {
-    // ======================= metadata: canonical nibbles -> tensor-core layout =======================
+    // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
-    // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3.
-    const int L = 32 * (warp - Cfg::W_META) + lane;
+    // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3. The warp
+    // writes its lane quarter (warp % 4) with tcgen05.st: no shared memory, no proxy fence.
+    const int qd = warp & 3;
+    const int L = 32 * qd + lane;
     const int m_a = (L & 7) + 16 * (L >> 4);
     const int k1 = (L >> 3) & 1;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(32 * qd) << 16);
     uint32_t wa[kPrefetch][4], wb[kPrefetch][4];
     auto fetch = [&](int it, uint32_t (&xa)[4], uint32_t (&xb)[4]) {
       if (it >= total) return;
       int m_tile, n_tile;
       tile_of(it / p.num_ks, m_tile, n_tile);
       const int ks = it % p.num_ks;
-      const int64_t ra = static_cast<int64_t>(m_tile) * 128 + m_a;
+      const int64_t ra = static_cast<int64_t>(m_tile) * 128 * CG + row_off + m_a;
       load_meta_stage(p, ra, ks, xa);
       load_meta_stage(p, ra + 8, ks, xb);
     };
@@ -413,11 +442,14 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           for (int kb = 0; kb < 4; ++kb)
             o[kb] = ((wa[j][kb] >> (16 * k1)) & 0xFFFFu) | (((wb[j][kb] >> (16 * k1)) & 0xFFFFu) << 16);
           mbar_wait(empty0 + 8 * stage, ((it / STAGES) & 1) ^ 1);
-          uint8_t* e_smem = smem + stage * Cfg::STAGE_BYTES + Cfg::A_BYTES + NB * Cfg::B_BYTES;
-          *reinterpret_cast<uint4*>(e_smem + 16 * L) = make_uint4(o[0], o[1], o[2], o[3]);
-          fence_proxy_async_smem();
+          tmem_st_32x32b_x4(lane_base + Cfg::E_COL + 4 * stage, o[0], o[1], o[2], o[3]);
+          tmem_st_wait();
+          tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(full0 + 8 * stage);
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(full0 + 8 * stage, 0));
+            else mbar_arrive(full0 + 8 * stage);
+          }
           fetch(it + kPrefetch, wa[j], wb[j]);
         }
       }
@@ -426,9 +458,11 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == Cfg::W_MMA) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_2sm<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
 }
 

@@ -62,6 +62,32 @@ venom_status_t launch_status() {
   return cudaGetLastError() == cudaSuccess ? VENOM_OK : VENOM_ERR_CUDA;
 }
 
+// Launch with an optional CTA-pair cluster (cg = 2 -> cluster dims {2,1,1}).
+template <typename Kern, typename... Args>
+venom_status_t launch_cg(Kern kern, int cg, int grid, int threads, int smem, cudaStream_t s,
+                         Args... args) {
+  if (cg == 1) {
+    kern<<<grid, threads, smem, s>>>(args...);
+    return launch_status();
+  }
+  grid -= grid % cg;
+  if (grid < cg) grid = cg;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, args...) != cudaSuccess) return VENOM_ERR_CUDA;
+  return launch_status();
+}
+
 // ------------------------------------------------------------------ SpMM dispatch
 template <class Cfg, bool kBF16>
 venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams p, int max_ctas,
@@ -74,11 +100,12 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  p.m_tiles = static_cast<int>((p.R + 128 * Cfg::CG - 1) / (128 * Cfg::CG));
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid < 1) return VENOM_OK;
-  kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tv, tb, p);
-  return launch_status();
+  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, p);
 }
 
 template <class Cfg>
@@ -285,7 +312,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
   const int V = f.v;
   const int64_t G = K / f.m;
-  const bool can_gather = (V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0);
+  const bool can_gather = (f.m == 4 || V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0);
   const bool can_densek = (f.m % 4 == 0) && (f.m <= 32) && (G % 4 == 0);
   const int strategy = opts ? opts->strategy : VENOM_STRATEGY_AUTO;
   if (strategy == VENOM_STRATEGY_GATHER && !can_gather) return VENOM_ERR_UNSUPPORTED_PATTERN;
@@ -394,25 +421,32 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return VENOM_ERR_CUDA;
   }
-  // B: 2-D [K rows][T] 16-bit, box 64 × 1 row (gather4 fetches 4 rows), 128B swizzle
-  if (!encode_b(&tb, 1)) return VENOM_ERR_CUDA;
+  // B: 2-D [K rows][T] 16-bit, 128B swizzle; box 64 × 1 row for gather4 (4 rows per op), or
+  // 64 × 128 rows when M = 4 (every group's 4 columns are selected: plain K-slices of B)
+  const bool contiguous = (f.m == 4);
+  if (!encode_b(&tb, contiguous ? 128 : 1)) return VENOM_ERR_CUDA;
   p.num_ks = static_cast<int>((G + 31) / 32);
-  if (tile_t == 0) tile_t = (NB == 1) ? 256 : (NB == 2 ? 128 : 64);
+  const int NBg = contiguous ? 1 : NB;  // M = 4 ignores V (column_idx is the identity)
+  const bool pair_ok = NBg == 1 && (contiguous || V % 256 == 0);
+  const int pair = (opts && opts->cta_pair) ? opts->cta_pair : (pair_ok ? 2 : 1);
+  if (pair == 2 && !pair_ok) return VENOM_ERR_INVALID_ARGUMENT;
+  if (tile_t == 0) tile_t = (NBg == 1) ? 256 : (NBg == 2 ? 128 : 64);
   set_tiles(tile_t);
-  if (NB == 1) {
+  if (NBg == 1 && pair == 2) {
+    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 4, 8, 2>>(bf16, tv, tb, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 6, 8, 2>>(bf16, tv, tb, p, max_ctas, s);
+  } else if (NBg == 1) {
     if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2>>(bf16, tv, tb, p, max_ctas, s);
     if (tile_t == 192) return run_spmm_dt<SpmmCfg<1, 192, 3>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 128) {
-      if (stages == 2) return run_spmm_dt<SpmmCfg<1, 128, 2>>(bf16, tv, tb, p, max_ctas, s);
-      return run_spmm_dt<SpmmCfg<1, 128, 4>>(bf16, tv, tb, p, max_ctas, s);
-    }
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 4>>(bf16, tv, tb, p, max_ctas, s);
     if (tile_t == 64) return run_spmm_dt<SpmmCfg<1, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
-  } else if (NB == 2) {
+  } else if (NBg == 2) {
     if (tile_t == 128) return run_spmm_dt<SpmmCfg<2, 128, 2>>(bf16, tv, tb, p, max_ctas, s);
     if (tile_t == 64) return run_spmm_dt<SpmmCfg<2, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
   } else {
     if (tile_t == 64) return run_spmm_dt<SpmmCfg<4, 64, 2>>(bf16, tv, tb, p, max_ctas, s);
   }
+  (void)stages;
   return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
 }
 

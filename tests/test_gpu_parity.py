@@ -207,7 +207,7 @@ SPMM_CASES = [
 def strategies(K, V, M):
     """Strategies applicable to a problem (include/venom.h): AUTO plus each forced one."""
     out = [venom.STRATEGY_AUTO]
-    if (V in (32, 64) or V % 128 == 0) and (K // M) % 4 == 0:
+    if (M == 4 or V in (32, 64) or V % 128 == 0) and (K // M) % 4 == 0:
         out.append(venom.STRATEGY_GATHER)
     if M in (4, 8, 16, 32) and (K // M) % 4 == 0:
         out.append(venom.STRATEGY_DENSE_K)
