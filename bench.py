@@ -153,7 +153,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- GPU workload
 class Layer:
-    def __init__(self, name, device, rank):
+    def __init__(self, name, device, rank, form="auto"):
         import paper_2310_02065_b200 as venom
         self.venom = venom
         self.name = name
@@ -165,6 +165,10 @@ class Layer:
         self.B = synth.gaussian_device((w["K"], w["T"]), 1.0, synth.F16, sb + 7919 * rank, device)
         self.bias = synth.gaussian_device((w["R"],), 0.5, synth.F16, sb + 1, device)
         self.x = venom.compress(self.A, V=w["V"], M=w["M"], check=True)
+        # execution form of the operand: the V:N:M arrays themselves, or the same matrix re-encoded
+        # as V:2:4 (dense-K, reading #18) when that runs faster on B200
+        self.expand = (form == "2to4") or (form == "auto" and venom.prefers_2to4(w["R"], w["K"], w["T"], w["V"], w["M"]))
+        self.y = venom.expand_2to4(self.x, check=True) if self.expand else self.x
         self.C = torch.empty((w["R"], w["T"]), dtype=torch.float16, device=device)
         self.D = torch.empty((w["R"], w["K"]), dtype=torch.float16, device=device)
         self.flops = useful_flops(w)
@@ -172,9 +176,11 @@ class Layer:
     def compress(self, A=None):
         w = self.w
         self.venom.compress(self.A if A is None else A, V=w["V"], M=w["M"], out=self.x)  # a1-a3
+        if self.expand:
+            self.venom.expand_2to4(self.x, out=self.y)
 
     def spmm(self, B=None, out=None, **kw):
-        return self.venom.spmm(self.x, self.B if B is None else B, bias=self.bias,
+        return self.venom.spmm(self.y, self.B if B is None else B, bias=self.bias,
                                out=self.C if out is None else out, **kw)  # a5-a9
 
     def decompress(self):
@@ -186,7 +192,7 @@ def run_gpu(args, ws, rank, local):
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     init_dist(ws, "nccl")
-    layers = [Layer(n, device, rank) for n in WORKLOAD_SETS[args.workload]]
+    layers = [Layer(n, device, rank, args.form) for n in WORKLOAD_SETS[args.workload]]
     kw = {}
     if args.tile_t:
         kw["tile_t"] = args.tile_t
@@ -218,7 +224,7 @@ def run_gpu(args, ws, rank, local):
             if part_events is not None:
                 part_events[3].record(stream)
 
-    launches_per_step = len(layers) * (3 if args.step == "full" else 2)
+    launches_per_step = sum((3 if args.step == "full" else 2) + int(L.expand) for L in layers)
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -338,6 +344,8 @@ def run_gpu(args, ws, rank, local):
             "config": {"workload": args.workload, "layers": [L.name for L in layers],
                        "V:N:M": f"{w0['V']}:2:{w0['M']}", "tokens_per_gpu": w0["T"],
                        "step": ("compress+spmm+decompress per layer" if args.step == "full" else "spmm per layer"),
+                       "operand_form": ["V:2:4 re-encoded (expand inside the step)" if L.expand else "V:N:M"
+                                        for L in layers],
                        "l2": "flushed (512 MiB write) before every timed step", "parallelism": f"T-split x{ws}"},
             "spmm_only": {"tflops": round(achieved, 3), "ms_per_launch": [round(x, 5) for x in per_launch_ms]},
             "step_breakdown_ms": {"compress_all_layers": round(compress_ms, 5),
@@ -441,6 +449,8 @@ def main(argv=None):
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--strategy", choices=["gather", "densek"], default=None,
                     help="force a venom_spmm strategy (default: the library's cost model)")
+    ap.add_argument("--form", choices=["auto", "vnm", "2to4"], default="auto",
+                    help="SpMM operand form: V:N:M as compressed, or re-encoded V:2:4 (venom_expand_2to4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

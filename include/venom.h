@@ -117,6 +117,31 @@ venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uin
                           const void* bias,
                           venom_dtype_t dt, venom_stream_t stream);
 
+/*
+ * Re-encode a V:N:M matrix with M % 4 == 0 as the SAME matrix in V:2:4 form over the original K
+ * (reading #18 "dense-K"): a group of M columns keeps 2 values, so each aligned 4-column
+ * subgroup holds at most 2 — the V:N:M pattern is a 2:4 pattern. Per row and 4-column subgroup:
+ * two kept values -> (a, b) at their positions; one kept value v at position i -> (v, 0) at (0, 1)
+ * if i == 0 else (0, v) at (0, i); none -> zeros at (0, 1) (inserted zeros are +0.0). Outputs are
+ * the canonical arrays of format {v, 2, 4}: values_out dtype[R][K/4][2], metadata_out
+ * uint8[R][ceil(K/8)], column_idx_out uint8[R/V][K/4][4] (all {0,1,2,3}). decompress(out) equals
+ * decompress(in) bit for bit, so venom_spmm on the output computes the same product — on B200 the
+ * M = 4 SpMM (dense B tiles, CTA pairs, no gathers) is the faster execution for small V·M.
+ * Corrupt metadata is reported through *dev_status (nullable).
+ */
+venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,
+                                const uint8_t* column_idx, int64_t R, int64_t K,
+                                venom_dtype_t dt, venom_format_t f,
+                                void* values_out, uint8_t* metadata_out, uint8_t* column_idx_out,
+                                int32_t* dev_status, venom_stream_t stream);
+
+/*
+ * Planner hint: 1 when venom_spmm over venom_expand_2to4's output is expected to run faster on
+ * B200 than venom_spmm on the V:N:M operand itself for this shape (R, K, T, f); 0 otherwise,
+ * including for any invalid format. Pure host function, no device access.
+ */
+int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f);
+
 /* Optional overrides for venom_spmm (benchmarking / tuning / ablation). Zero = library default.
  *   tile_t    output columns per CTA tile (64, 128, 192 or 256; availability depends on strategy)
  *   stages    pipeline depth (where a variant exists)

@@ -64,6 +64,7 @@ def _load():
         lib.oracle_spmm_compressed.argtypes = [P, P, P, I64, I64, I, I, I, I, P, I64, I64, P, P, I64]
         lib.oracle_gemm_dense.argtypes = [P, I64, I64, I64, I, P, I64, I64, P, P, I64]
         lib.oracle_num_threads.argtypes = []
+        lib.oracle_expand_2to4.argtypes = [P, P, P, I64, I64, I, I, I, P, P, P]
         _lib = lib
     return _lib
 
@@ -121,6 +122,23 @@ def decompress(values, metadata, column_idx, R: int, K: int, dtype: int, V: int,
             raise OracleError(st, "decompress")
         return st
     return out
+
+
+def expand_2to4(values, metadata, column_idx, R: int, K: int, V: int, M: int, N: int = 2,
+                check: bool = True):
+    """V:N:M (M % 4 == 0) -> the same matrix as V:2:4 over the original K (see the C source)."""
+    G2 = K // 4
+    v2 = np.zeros((R, G2, 2), np.uint16)
+    m2 = np.zeros((R, (G2 + 1) // 2), np.uint8)
+    c2 = np.zeros((R // V, G2, 4), np.uint8)
+    st = _load().oracle_expand_2to4(_ptr(np.ascontiguousarray(values)), _ptr(np.ascontiguousarray(metadata)),
+                                    _ptr(np.ascontiguousarray(column_idx)), R, K, V, N, M,
+                                    _ptr(v2), _ptr(m2), _ptr(c2))
+    if st != OK:
+        if check:
+            raise OracleError(st, "expand_2to4")
+        return st
+    return v2, m2, c2
 
 
 def spmm(values, metadata, column_idx, R: int, K: int, dtype: int, V: int, M: int,

@@ -275,6 +275,73 @@ int oracle_gemm_dense(const uint16_t* A, int64_t R, int64_t K, int64_t lda, int 
   return ORC_OK;
 }
 
+/*
+ * Re-encoding of a V:N:M matrix (M % 4 == 0) as a V:2:4 matrix over the ORIGINAL K (the "dense-K"
+ * execution plan, reading #18). A group of M columns keeps 2 values, so every aligned
+ * 4-column subgroup of it holds at most 2 kept positions: the V:N:M pattern is a 2:4 pattern. Per
+ * row and 4-column subgroup j (columns 4j..4j+3), take the kept positions of the V:N:M structure
+ * that fall inside it (from column_idx and the m-indices — the structure, not the values):
+ *   two kept  -> values (a, b) at positions (i0, i1), i0 < i1
+ *   one kept  -> position i: (v, 0) at (0, 1) if i == 0, else (0, v) at (0, i)
+ *   none      -> (0, 0) at (0, 1)
+ * where an inserted 0 is +0.0 (bits 0x0000) and kept values keep their original bits. The output
+ * column_idx is the identity [0,1,2,3] for every block. Outputs: values2 R x (K/4) x 2,
+ * metadata2 R x ceil((K/4)/2), column_idx2 (R/V) x (K/4) x 4.
+ */
+int oracle_expand_2to4(const uint16_t* values, const uint8_t* metadata, const uint8_t* column_idx,
+                       int64_t R, int64_t K, int V, int N, int M,
+                       uint16_t* values2, uint8_t* metadata2, uint8_t* column_idx2) {
+  int st = oracle_validate(R, K, V, N, M);
+  if (st != ORC_OK) return st;
+  if (M % 4 != 0) return ORC_UNSUPPORTED_PATTERN;
+  const int64_t G = K / M, meta_row = (G + 1) / 2;
+  const int64_t G2 = K / 4, meta_row2 = (G2 + 1) / 2;
+  if (!column_idx_ok(column_idx, R, V, G, M)) return ORC_CORRUPT_METADATA;
+  memset(metadata2, 0, (size_t)(R * meta_row2));
+  for (int64_t b = 0; b < (R / V) * G2; ++b) {
+    for (int t = 0; t < 4; ++t) column_idx2[b * 4 + t] = (uint8_t)t;
+  }
+  for (int64_t i = 0; i < R; ++i) {
+    const int64_t rb = i / V;
+    for (int64_t g = 0; g < G; ++g) {
+      int p[2];
+      if (nib_positions(metadata, meta_row, i, g, &p[0], &p[1])) return ORC_CORRUPT_METADATA;
+      /* absolute columns of the two kept values, ascending (column_idx and m-indices ascend) */
+      int64_t col[2];
+      uint16_t val[2];
+      for (int s2 = 0; s2 < 2; ++s2) {
+        col[s2] = g * M + column_idx[(rb * G + g) * 4 + p[s2]];
+        val[s2] = values[(i * G + g) * 2 + s2];
+      }
+      for (int64_t j = g * (M / 4); j < (g + 1) * (M / 4); ++j) {   /* subgroups of this group */
+        int n = 0, pos[2];
+        uint16_t v[2];
+        for (int s2 = 0; s2 < 2; ++s2) {
+          if (col[s2] >= 4 * j && col[s2] < 4 * j + 4) {
+            pos[n] = (int)(col[s2] - 4 * j);
+            v[n] = val[s2];
+            ++n;
+          }
+        }
+        uint16_t out0, out1;
+        int q0, q1;
+        if (n == 2) {
+          out0 = v[0]; out1 = v[1]; q0 = pos[0]; q1 = pos[1];
+        } else if (n == 1) {
+          if (pos[0] == 0) { out0 = v[0]; out1 = 0x0000; q0 = 0; q1 = 1; }
+          else             { out0 = 0x0000; out1 = v[0]; q0 = 0; q1 = pos[0]; }
+        } else {
+          out0 = 0x0000; out1 = 0x0000; q0 = 0; q1 = 1;
+        }
+        values2[(i * G2 + j) * 2 + 0] = out0;
+        values2[(i * G2 + j) * 2 + 1] = out1;
+        metadata2[i * meta_row2 + j / 2] |= (uint8_t)((q0 | (q1 << 2)) << (4 * (j % 2)));
+      }
+    }
+  }
+  return ORC_OK;
+}
+
 /* Number of OpenMP threads the parallel loops above use (1 when built without OpenMP). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

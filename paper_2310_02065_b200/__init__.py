@@ -30,7 +30,8 @@ STATUS_NAMES = {
     8: "VENOM_ERR_ARCH", 9: "VENOM_ERR_CUDA",
 }
 EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
-            "venom_spmm_ex", "venom_kernels_per_call", "venom_status_string", "venom_version"]
+            "venom_spmm_ex", "venom_expand_2to4", "venom_prefer_2to4", "venom_kernels_per_call", "venom_status_string",
+            "venom_version"]
 
 
 class VenomError(RuntimeError):
@@ -67,10 +68,13 @@ def lib() -> ctypes.CDLL:
         L.venom_compress.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P]
         L.venom_decompress.argtypes = [P, P, P, I64, I64, ctypes.c_int, _Format, P, I64, P, P]
         L.venom_spmm.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int, P]
+        L.venom_expand_2to4.argtypes = [P, P, P, I64, I64, ctypes.c_int, _Format, P, P, P, P, P]
+        L.venom_prefer_2to4.argtypes = [I64, I64, I64, _Format]
+        L.venom_prefer_2to4.restype = ctypes.c_int
         L.venom_spmm_ex.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int,
                                     ctypes.POINTER(_Opts), P]
         for fn in ("venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
-                   "venom_spmm_ex"):
+                   "venom_spmm_ex", "venom_expand_2to4"):
             getattr(L, fn).restype = ctypes.c_int
         L.venom_status_string.argtypes = [ctypes.c_int]
         L.venom_status_string.restype = ctypes.c_char_p
@@ -204,6 +208,36 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
                              _dt(x.dtype), ctypes.byref(opts), _stream(B.device))
     _check(st, "venom_spmm")
     return out
+
+
+def expand_2to4(x: VNMTensor, out: Optional[VNMTensor] = None, status: Optional[torch.Tensor] = None,
+                check: bool = False) -> VNMTensor:
+    """The same matrix as V:2:4 over the original K (M % 4 == 0): the dense-K execution form."""
+    R, K, V = x.R, x.K, x.V
+    G2 = K // 4
+    dev = x.values.device
+    if out is None:
+        out = VNMTensor(torch.empty((R, G2, 2), dtype=x.dtype, device=dev),
+                        torch.empty((R, (G2 + 1) // 2), dtype=torch.uint8, device=dev),
+                        torch.empty((R // V, G2, 4), dtype=torch.uint8, device=dev), R, K, V, 4)
+    if check and status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = lib().venom_expand_2to4(ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
+                                 ctypes.c_void_p(x.column_idx.data_ptr()), R, K, _dt(x.dtype), x.fmt(),
+                                 ctypes.c_void_p(out.values.data_ptr()), ctypes.c_void_p(out.metadata.data_ptr()),
+                                 ctypes.c_void_p(out.column_idx.data_ptr()),
+                                 ctypes.c_void_p(status.data_ptr() if status is not None else 0),
+                                 _stream(dev))
+    _check(st, "venom_expand_2to4")
+    if check:
+        _check(int(status.item()), "venom_expand_2to4 (device status)")
+    return out
+
+
+def prefers_2to4(R: int, K: int, T: int, V: int, M: int) -> bool:
+    """Whether the library's planner runs this shape faster as the V:2:4 re-encoding (expand_2to4)
+    than straight on the V:N:M operand (venom_prefer_2to4)."""
+    return bool(lib().venom_prefer_2to4(R, K, T, _Format(V, 2, M)))
 
 
 def version() -> str:

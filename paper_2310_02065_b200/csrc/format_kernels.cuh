@@ -273,4 +273,64 @@ __global__ void __launch_bounds__(256) vnm_decompress_kernel(
   if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
 }
 
+// Re-encoding V:N:M (M % 4 == 0) -> V:2:4 over the original K (reading #18; the oracle's
+// oracle_expand_2to4 states the rules). grid (pairs of groups, rows); thread per (row, 2 groups):
+// the kept positions of each group are resolved through column_idx and the m-indices, and every
+// 4-column subgroup is written as two values + one nibble. The output column_idx is the identity.
+__global__ void __launch_bounds__(256) vnm_expand_2to4_kernel(
+    const uint32_t* __restrict__ values, const uint8_t* __restrict__ metadata,
+    const uint32_t* __restrict__ column_idx, int64_t R, int V, int M, int64_t G,
+    uint32_t* __restrict__ values2, uint8_t* __restrict__ metadata2,
+    uint32_t* __restrict__ column_idx2, int32_t* __restrict__ status) {
+  const int64_t npairs = (G + 1) / 2;
+  const int64_t pp = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pp >= npairs) return;
+  const int sub = M / 4;                       // subgroups per group
+  const int64_t G2 = G * sub, meta_row = (G + 1) / 2, meta_row2 = (G2 + 1) / 2;
+  bool bad = false;
+  for (int64_t row = blockIdx.y; row < R; row += gridDim.y) {
+    const int64_t rb = row / V;
+    uint32_t acc = 0;   // pending nibbles of the current output byte
+    for (int h = 0; h < 2; ++h) {
+      const int64_t g = 2 * pp + h;
+      if (g >= G) break;
+      const uint32_t cw = __ldg(column_idx + rb * G + g);
+      const uint32_t nib = (__ldg(metadata + row * meta_row + (g >> 1)) >> (4 * (g & 1))) & 0xFu;
+      const uint32_t p0 = nib & 3u, p1 = nib >> 2;
+      bad |= !(p0 < p1) || ((cw >> 24) >= static_cast<uint32_t>(M));
+      const int c0 = static_cast<int>((cw >> (8 * p0)) & 0xFFu);
+      const int c1 = static_cast<int>((cw >> (8 * p1)) & 0xFFu);
+      const uint32_t v = __ldg(values + row * G + g);
+      for (int u = 0; u < sub; ++u) {
+        const int j0 = 4 * u;
+        const bool in0 = (c0 >= j0 && c0 < j0 + 4), in1 = (c1 >= j0 && c1 < j0 + 4);
+        uint32_t w, nb;
+        if (in0 && in1) {
+          w = v;
+          nb = static_cast<uint32_t>(c0 - j0) | (static_cast<uint32_t>(c1 - j0) << 2);
+        } else if (in0 || in1) {
+          const uint32_t x = in0 ? (v & 0xFFFFu) : (v >> 16);
+          const uint32_t i = static_cast<uint32_t>((in0 ? c0 : c1) - j0);
+          w = (i == 0u) ? x : (x << 16);
+          nb = (i == 0u) ? 0x4u : (i << 2);
+        } else {
+          w = 0u;
+          nb = 0x4u;
+        }
+        const int64_t j = g * sub + u;
+        values2[row * G2 + j] = w;
+        if (j & 1) {
+          metadata2[row * meta_row2 + (j >> 1)] = static_cast<uint8_t>(acc | (nb << 4));
+          acc = 0;
+        } else {
+          acc = nb;
+          if (j == G2 - 1) metadata2[row * meta_row2 + (j >> 1)] = static_cast<uint8_t>(acc);
+        }
+        if (row % V == 0) column_idx2[rb * G2 + j] = 0x03020100u;
+      }
+    }
+  }
+  if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
+}
+
 }  // namespace venom

@@ -303,6 +303,41 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
   return launch_status();
 }
 
+int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f) {
+  if (validate_format(R, K, f) != VENOM_OK || f.m % 4 != 0 || f.m == 4) return 0;
+  if ((K / 4) % 4 != 0 || T < 256) return 0;
+  // measured crossover: the gathered path is bound by the gather feed,
+  // whose bytes per useful FLOP grow as 1/V, while the 2:4 CTA-pair path streams dense B tiles
+  // at twice the useful work; below V·M ≈ 1536 the 2:4 form wins
+  return static_cast<int64_t>(f.v) * f.m <= 1536 ? 1 : 0;
+}
+
+venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,
+                                const uint8_t* column_idx, int64_t R, int64_t K, venom_dtype_t dt,
+                                venom_format_t f, void* values_out, uint8_t* metadata_out,
+                                uint8_t* column_idx_out, int32_t* dev_status,
+                                venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (f.m % 4 != 0) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!values || !metadata || !column_idx || !values_out || !metadata_out || !column_idx_out)
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(values, 4) || !aligned(column_idx, 4) || !aligned(values_out, 4) ||
+      !aligned(column_idx_out, 4))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  const int64_t npairs = (G + 1) / 2;
+  const dim3 grid(static_cast<unsigned>((npairs + 255) / 256), static_cast<unsigned>(R < 65535 ? R : 65535));
+  venom::vnm_expand_2to4_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint32_t*>(values), metadata, reinterpret_cast<const uint32_t*>(column_idx), R,
+      f.v, f.m, G, static_cast<uint32_t*>(values_out), metadata_out,
+      reinterpret_cast<uint32_t*>(column_idx_out), dev_status);
+  return launch_status();
+}
+
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
                              int64_t R, int64_t K, venom_format_t f, const void* B, int64_t T,
                              int64_t ldb, void* C, int64_t ldc, const void* bias, venom_dtype_t dt,

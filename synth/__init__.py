@@ -25,6 +25,11 @@ WORKLOADS = {
     "sweep_4096x4096x4096_128:2:16": dict(R=4096, K=4096, T=4096, V=128, M=16, cfg=2),
     "sweep_4096x4096x4096_128:2:32": dict(R=4096, K=4096, T=4096, V=128, M=32, cfg=2),
     "sweep_4096x4160x4096_128:2:40": dict(R=4096, K=4160, T=4096, V=128, M=40, cfg=2),
+    "sweep_4096x4096x4096_64:2:4": dict(R=4096, K=4096, T=4096, V=64, M=4, cfg=2),
+    "sweep_4096x4096x4096_64:2:8": dict(R=4096, K=4096, T=4096, V=64, M=8, cfg=2),
+    "sweep_4096x4096x4096_64:2:16": dict(R=4096, K=4096, T=4096, V=64, M=16, cfg=2),
+    "sweep_4096x4096x4096_64:2:32": dict(R=4096, K=4096, T=4096, V=64, M=32, cfg=2),
+    "sweep_4096x4160x4096_64:2:40": dict(R=4096, K=4160, T=4096, V=64, M=40, cfg=2),
     "gpt3_ffn_12288x49152x8192_128:2:16": dict(R=12288, K=49152, T=8192, V=128, M=16, cfg=3),
 }
 

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared_symbols():
     src = open(os.path.join(ROOT, "include", "venom.h")).read()
-    return sorted(set(re.findall(r"\b(venom_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(venom_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -57,6 +57,20 @@ def _spmm(L, R=256, K=512, V=128, M=8, T=64, ldb=64, ldc=64, n=2, dt=0):
     fake = P(0x10000)  # never dereferenced: validation fails first
     return L.venom_spmm(fake, fake, fake, R, K, venom._Format(V, n, M), fake, T, ldb, fake, ldc,
                         P(0), dt, P(0))
+
+
+def test_expand_argument_errors(L):
+    P = ctypes.c_void_p
+    fake = P(0x10000)
+
+    def ex(R=256, K=512, V=64, M=8, dt=0, n=2):
+        return L.venom_expand_2to4(fake, fake, fake, R, K, dt, venom._Format(V, n, M), fake, fake, fake,
+                                   P(0), P(0))
+    assert ex(M=10, K=500) == 4   # M % 4 != 0: no 2:4 re-encoding
+    assert ex(R=200) == 2         # V does not divide R
+    assert ex(K=500) == 3         # M does not divide K
+    assert ex(dt=3) == 5
+    assert ex(n=1) == 4
 
 
 def test_spmm_argument_errors(L):

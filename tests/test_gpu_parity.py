@@ -142,6 +142,48 @@ def test_decompress_corrupt_metadata_status():
     assert e.value.status == 7
 
 
+# ------------------------------------------------------------------ V:N:M -> V:2:4 re-encoding: bit-exact
+EXPAND_CASES = [c for c in CASES if c[3] % 4 == 0] + [
+    (64, 8 * 7, 32, 8, "gauss", F16),      # odd G: last metadata byte half used
+    (32, 4 * 9, 16, 4, "int", BF16),       # M = 4, odd G2
+    (64, 96 * 3, 64, 96, "sparse", F16),   # most subgroups empty
+]
+
+
+@pytest.mark.parametrize("R,K,V,M,kind,dt", EXPAND_CASES)
+def test_expand_2to4_bit_exact(R, K, V, M, kind, dt):
+    A = make_input(R, K, kind, dt, 11 + R + K, M)
+    parts = oracle.compress(A, dt, V=V, M=M)
+    v2, m2, c2 = oracle.expand_2to4(*parts, R, K, V, M)
+    y = venom.expand_2to4(vnm_from(parts, R, K, V, M, dt), check=True)
+    assert (y.V, y.M, y.K) == (V, 4, K)
+    assert np.array_equal(to_bits(y.values), v2)
+    assert np.array_equal(y.metadata.cpu().numpy(), m2)
+    assert np.array_equal(y.column_idx.cpu().numpy(), c2)
+    # and the re-encoded operand decompresses to the original sparse matrix on the GPU
+    assert np.array_equal(to_bits(venom.decompress(y, check=True)),
+                          oracle.decompress(*parts, R, K, dt, V, M))
+
+
+def test_expand_2to4_then_spmm_matches_oracle():
+    R, K, T, V, M, dt = 512, 1024, 384, 64, 8, F16
+    A, B, _, parts = oracle_problem(R, K, T, V, M, dt, 77)
+    y = venom.expand_2to4(vnm_from(parts, R, K, V, M, dt), check=True)
+    C = venom.spmm(y, to_dev(B, dt))
+    torch.cuda.synchronize()
+    check_spmm(C, oracle.spmm(*parts, R, K, dt, V, M, B), dt)
+
+
+def test_expand_2to4_corrupt_metadata_status():
+    R, K, V, M = 64, 64, 32, 8
+    parts = list(oracle.compress(synth.gaussian((R, K), 1.0, F16, 9), F16, V=V, M=M))
+    parts[1] = parts[1].copy()
+    parts[1][3, 1] = 0x05  # p0 == p1
+    with pytest.raises(venom.VenomError) as e:
+        venom.expand_2to4(vnm_from(parts, R, K, V, M, F16), check=True)
+    assert e.value.status == 7
+
+
 # ------------------------------------------------------------------ SpMM
 def oracle_problem(R, K, T, V, M, dt, seed, bias=False, kind="gauss"):
     A = make_input(R, K, kind, dt, seed, M) if kind != "gauss" else synth.gaussian((R, K), 0.02, dt, seed)

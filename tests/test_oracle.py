@@ -300,3 +300,48 @@ def test_cost_identities():
         assert (R * K) / nv == ideal
     nv, _, nc = oracle.sizes(16, 32, 4, 8)
     assert nv / 16 == 32 / 4 and nc == (16 // 4) * (32 // 8) * 4   # B rows fetched per block: 4 of 8
+
+
+# --------------------------------------------------------------------------- 2:4 re-encoding
+@pytest.mark.parametrize("V,M,R,K,kind", [(64, 8, 128, 256, "gauss"), (4, 16, 16, 128, "int"),
+                                          (2, 4, 8, 64, "special"), (8, 32, 16, 256, "gauss"),
+                                          (16, 12, 32, 96, "int"), (1, 8, 8, 64, "special")])
+def test_expand_2to4_is_same_matrix(V, M, R, K, kind):
+    """expand(x) re-encodes the V:N:M matrix as V:2:4 over K (reading #18): the dense
+    matrices are bit-identical, the result is a valid 2:4 structure, and M = 4 is the identity."""
+    dt = F16
+    A = {"gauss": synth.gaussian((R, K), 1.0, dt, 5), "int": synth.small_integers((R, K), dt, 6),
+         "special": synth.special_values((R, K), dt, 7)}[kind]
+    vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
+    v2, m2, c2 = oracle.expand_2to4(vals, meta, cidx, R, K, V, M)
+    assert (c2 == np.array([0, 1, 2, 3], np.uint8)).all()
+    d1 = oracle.decompress(vals, meta, cidx, R, K, dt, V, M)
+    d2 = oracle.decompress(v2, m2, c2, R, K, dt, V, 4)
+    assert np.array_equal(d1, d2)
+    # the kept positions of the 2:4 form are a superset of the V:N:M kept positions
+    mask1 = mask_from_compressed(meta, cidx, R, K, V, M)
+    mask2 = mask_from_compressed(m2, c2, R, K, V, 4)
+    assert (mask2 | ~mask1).all() and mask2.sum() == R * K // 2
+    # SpMM through either encoding is the same product (exactly: one formulation, same terms)
+    B = synth.gaussian((K, 8), 1.0, dt, 8)
+    assert np.array_equal(oracle.spmm(vals, meta, cidx, R, K, dt, V, M, B),
+                          oracle.spmm(v2, m2, c2, R, K, dt, V, 4, B)) or \
+        rel_fro(oracle.spmm(vals, meta, cidx, R, K, dt, V, M, B), oracle.spmm(v2, m2, c2, R, K, dt, V, 4, B)) < 1e-15
+
+
+def test_expand_2to4_m4_identity_and_rules():
+    """M = 4: expand is the identity on (values, metadata). Hand case (M = 8, one row): kept columns
+    1 and 6 fall in different subgroups -> (0, a) at (0, 1) and (b, 0)... worked by hand below."""
+    A = synth.gaussian((8, 32), 1.0, F16, 9)
+    vals, meta, cidx = oracle.compress(A, F16, V=4, M=4)
+    v2, m2, _ = oracle.expand_2to4(vals, meta, cidx, 8, 32, 4, 4)
+    assert np.array_equal(v2, vals) and np.array_equal(m2, meta)
+    # one V:N:M group of 8 columns, column_idx [1,2,5,6], m-indices (0,3) -> kept columns 1 and 6
+    a, b = f64_to_bits(np.array([1.5, -2.0]), F16)
+    vals = np.array([[[a, b]]], np.uint16)
+    meta = np.array([[0x0C]], np.uint8)
+    cidx = np.array([[[1, 2, 5, 6]]], np.uint8)
+    v2, m2, _ = oracle.expand_2to4(vals, meta, cidx, 1, 8, 1, 8)
+    # subgroup 0 (cols 0-3): a at position 1 -> (0, a) at (0, 1); subgroup 1 (cols 4-7): b at 2 -> (0, b) at (0, 2)
+    assert v2.tolist() == [[[0, int(a)], [0, int(b)]]]
+    assert m2.tolist() == [[(0 | 1 << 2) | ((0 | 2 << 2) << 4)]]
