@@ -163,7 +163,7 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
       mbar_wait(full0 + 8 * stage, (it / STAGES) & 1);
       tc_fence_after();
       if (lane == 0) VENOM_TRACE_EVENT(1, it);
-      if (lane == 0) {
+      if (lane == 0 && !(p.dbg & 2)) {  // ablation 2: no MMAs (commits only)
         const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
         const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * stage;
 #pragma unroll
@@ -186,9 +186,14 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
                             (ks | kb) != 0 ? 1u : 0u);
           }
         }
+      }
+      if (lane == 0) {
         if constexpr (CG == 2) {
           tc_commit_2sm_mc(empty0 + 8 * stage, 0x3);
           if (ks == p.num_ks - 1) tc_commit_2sm_mc(accf0 + 8 * ab, 0x3);
+        } else if (p.dbg & 512) {  // ablation 512 (with 2): plain arrives instead of commits
+          mbar_arrive(empty0 + 8 * stage);
+          if (ks == p.num_ks - 1) mbar_arrive(accf0 + 8 * ab);
         } else {
           tc_commit(empty0 + 8 * stage);
           if (ks == p.num_ks - 1) tc_commit(accf0 + 8 * ab);
@@ -228,10 +233,15 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t v[32];
-      tmem_ld_32x32b_x32(t_row + 32 * c, v);
-      tmem_ld_wait();
+      if (p.dbg & 64) {  // ablation 64: no accumulator reads
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = 0u;
+      } else {
+        tmem_ld_32x32b_x32(t_row + 32 * c, v);
+        tmem_ld_wait();
+      }
       const int64_t col = col_base + 32 * c;
-      if (row < p.R) {
+      if (row < p.R && !(p.dbg & 4)) {  // ablation 4: no C stores
         uint16_t* dst = p.C + row * p.ldc + col;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -280,7 +290,8 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full0 + 8 * s, 1 + 4 * CG);  // leader's expect_tx + metadata warps of the pair
+      // leader's expect_tx + metadata warps of the pair (ablation 256: metadata warps idle)
+      mbar_init(full0 + 8 * s, (p.dbg & 256) ? 1 : 1 + 4 * CG);
       mbar_init(empty0 + 8 * s, 1);          // (multicast) MMA commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -364,11 +375,15 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           const int arow = m_tile * 128 * CG + row_off;
           if (warp == 0 && lane == 0) {
             VENOM_TRACE_EVENT(0, it);
-            if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, CG * Cfg::TX_BYTES);
-            if constexpr (CG == 2) tma_load_2d_2sm(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
-            else tma_load_2d(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+            // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load
+            const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES));
+            if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
+            if (!(p.dbg & 16)) {
+              if constexpr (CG == 2) tma_load_2d_2sm(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+              else tma_load_2d(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+            }
           }
-          if (contiguous && lane == 0) {
+          if (contiguous && lane == 0 && !(p.dbg & 1)) {
             // M = 4: the 4 "selected" rows of every group are the group itself — plain tile boxes,
             // one per 64-column chunk, issued by different warps (TMA issue is per-warp serial)
 #pragma unroll
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
                 else tma_load_2d(bdst, &tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
               }
           }
-          if (!contiguous) {
+          if (!contiguous && !(p.dbg & 1)) {
 #pragma unroll
             for (int j = 0; j < Cfg::LANE_OPS; ++j) {
               int b, c, q;
@@ -401,6 +416,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
             }
           }
           __syncwarp();
+          if (warp == 0 && lane == 0) VENOM_TRACE_EVENT(4, it);
           fetch(it + kPrefetch, cw[jj]);
         }
       }
@@ -416,6 +432,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     // writes its lane quarter (warp % 4) with tcgen05.st: no shared memory, no proxy fence.
     const int qd = warp & 3;
     const int L = 32 * qd + lane;
+    const int total_meta = (p.dbg & 256) ? 0 : total;
     const int m_a = (L & 7) + 16 * (L >> 4);
     const int k1 = (L >> 3) & 1;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(32 * qd) << 16);
@@ -426,12 +443,17 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
       tile_of(it / p.num_ks, m_tile, n_tile);
       const int ks = it % p.num_ks;
       const int64_t ra = static_cast<int64_t>(m_tile) * 128 * CG + row_off + m_a;
+      if (p.dbg & 32) {  // ablation 32: no metadata global loads
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) xa[kb] = xb[kb] = 0x44444444u;
+        return;
+      }
       load_meta_stage(p, ra, ks, xa);
       load_meta_stage(p, ra + 8, ks, xb);
     };
 #pragma unroll
     for (int j = 0; j < kPrefetch; ++j) fetch(j, wa[j], wb[j]);
-    for (int it0 = 0; it0 < total; it0 += kPrefetch) {
+    for (int it0 = 0; it0 < total_meta; it0 += kPrefetch) {
 #pragma unroll
       for (int j = 0; j < kPrefetch; ++j) {
         const int it = it0 + j;
@@ -442,11 +464,14 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           for (int kb = 0; kb < 4; ++kb)
             o[kb] = ((wa[j][kb] >> (16 * k1)) & 0xFFFFu) | (((wb[j][kb] >> (16 * k1)) & 0xFFFFu) << 16);
           mbar_wait(empty0 + 8 * stage, ((it / STAGES) & 1) ^ 1);
-          tmem_st_32x32b_x4(lane_base + Cfg::E_COL + 4 * stage, o[0], o[1], o[2], o[3]);
-          tmem_st_wait();
+          if (!(p.dbg & 8)) {  // ablation 8: no metadata stores
+            tmem_st_32x32b_x4(lane_base + Cfg::E_COL + 4 * stage, o[0], o[1], o[2], o[3]);
+            tmem_st_wait();
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
+            if (qd == 0) VENOM_TRACE_EVENT(3, it);
             if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(full0 + 8 * stage, 0));
             else mbar_arrive(full0 + 8 * stage);
           }

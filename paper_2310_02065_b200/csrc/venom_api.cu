@@ -182,22 +182,6 @@ venom_status_t run_densek_m(int M, bool bf16, const CUtensorMap& tb, EncodeTiled
 // feed time) with the feed rates measured by tools/microbench.cu on B200 (gather of 128-byte rows
 // ~31 B/cycle/SM; 16 KB TMA boxes ~55 B/cycle/SM) and the sparse MMA issue rate (~13k dense-
 // equivalent FLOP/cycle/SM at N = 256). Returns relative costs in cycles·SM.
-double cost_gather(int64_t R, int64_t K, int64_t T, int V, int M, int bn) {
-  const double G = double(K / M), Kp = 4.0 * G;
-  const int NB = (V % 128 == 0) ? 1 : 128 / V;
-  const double mtiles = double((R + 127) / 128), ntiles = double((T + bn - 1) / bn);
-  const double bytes = mtiles * NB * Kp * double(T) * 2.0 + double(R) * 2.0 * G * 2.0 * ntiles;
-  const double mma = mtiles * NB * 2.0 * 128.0 * Kp * double(T);
-  return bytes / 31.0 > mma / 13000.0 ? bytes / 31.0 : mma / 13000.0;
-}
-double cost_densek(int64_t R, int64_t K, int64_t T, int M, int bn) {
-  const double G = double(K / M);
-  const double mtiles = double((R + 127) / 128), ntiles = double((T + bn - 1) / bn);
-  const double bytes = mtiles * double(K) * double(T) * 2.0 + double(R) * G * 4.5 * ntiles;
-  const double mma = mtiles * 2.0 * 128.0 * double(K) * double(T);
-  return bytes / 55.0 > mma / 13000.0 ? bytes / 55.0 : mma / 13000.0;
-}
-
 }  // namespace
 
 extern "C" {
@@ -388,7 +372,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   else if (strategy == VENOM_STRATEGY_DENSE_K) use_densek = true;
   else if (!can_gather) use_densek = true;
   else if (!can_densek) use_densek = false;
-  else use_densek = cost_densek(R, K, T, f.m, 256) < cost_gather(R, K, T, V, f.m, NB == 1 ? 256 : 128);
+  else use_densek = false;  // measured: the gathered / contiguous kernel wins wherever it applies
 
   SpmmParams p;
   p.values = static_cast<const uint16_t*>(values);

@@ -54,18 +54,21 @@ int main(int argc, char** argv) {
   for (int k = 0; k < 16; ++k)
     for (int i = 0; i < 256; ++i)
       if (h[k * 256 + i] && h[k * 256 + i] < t0) t0 = h[k * 256 + i];
-  const char* names[8] = {"prodB", "mmaFull", "mmaCommit", "expRaw", "expEmpty", "expArrive", "", ""};
-  printf("it ");
-  for (int k = 0; k < 6; ++k) printf("%10s", names[k]);
-  printf("   (ns since first event, CTA 0)\n");
-  for (int i = 0; i < 64; ++i) {
-    printf("%3d", i);
-    for (int k = 0; k < 6; ++k) {
-      const unsigned long long v = h[k * 256 + i];
-      if (v) printf("%10llu", v - t0);
-      else printf("%10s", "-");
+  const char* names[8] = {"prodB", "mmaFull", "mmaCommit", "meta/expRaw", "prodDone/expEmpty",
+                          "expArrive", "", ""};
+  for (int cta = 0; cta < 2; ++cta) {
+    printf("CTA %d\nit ", cta);
+    for (int k = 0; k < 6; ++k) printf("%18s", names[k]);
+    printf("   (ns since first event)\n");
+    for (int i = 0; i < 80; ++i) {
+      printf("%3d", i);
+      for (int k = 0; k < 6; ++k) {
+        const unsigned long long v = h[(cta * 16 + k) * 256 + i];
+        if (v) printf("%18llu", v - t0);
+        else printf("%18s", "-");
+      }
+      printf("\n");
     }
-    printf("\n");
   }
   return 0;
 }
