@@ -1,0 +1,90 @@
+"""World-size-2 tests of the multi-GPU host logic on CPU (gloo): bench.py's rank environment,
+max-over-ranks timing, weak-scaling aggregation, rank-0-only reference arm, and the T-split of the
+SpMM: column shards of B computed independently and concatenated equal the
+unsharded product bit for bit (checked with the oracle, no GPU)."""
+from __future__ import annotations
+
+import io
+import os
+import socket
+import sys
+from contextlib import redirect_stdout
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, ws: int, port: int, q):
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                          WORLD_SIZE=str(ws), LOCAL_RANK=str(rank))
+        import bench
+        import oracle
+        import synth
+        env = bench.dist_env()
+        assert env == (ws, rank, rank), env
+        bench.init_dist(ws, "gloo")
+        # max over ranks and weak-scaling aggregation
+        t = bench.max_over_ranks(0.5 + rank, ws)
+        assert t == 0.5 + (ws - 1)
+        assert bench.aggregate(10.0, ws, t) == pytest.approx(10.0 * ws / t)
+        bench.barrier(ws)
+
+        # T-split: rank r owns columns [r*T/ws, (r+1)*T/ws) of one global B; no collective on the
+        # SpMM itself, the all_gather below only collects the result for the check
+        R, K, T, V, M = 64, 128, 96, 32, 8
+        A = synth.gaussian((R, K), 0.02, synth.F16, 5)
+        B = synth.gaussian((K, T), 1.0, synth.F16, 6)
+        parts = oracle.compress(A, synth.F16, V=V, M=M)
+        ts = T // ws
+        C_r = oracle.spmm(*parts, R, K, synth.F16, V, M, np.ascontiguousarray(B[:, rank * ts:(rank + 1) * ts]))
+        gathered = [torch.empty((R, ts), dtype=torch.float64) for _ in range(ws)]
+        dist.all_gather(gathered, torch.from_numpy(C_r))
+        if rank == 0:
+            C_full = oracle.spmm(*parts, R, K, synth.F16, V, M, B)
+            C_cat = torch.cat(gathered, dim=1).numpy()
+            assert np.array_equal(C_cat, C_full)
+
+        # weak scaling draws per-rank activations: the ranks' B differ
+        b_r = torch.from_numpy(synth.gaussian((8, 8), 1.0, synth.F16, 1001 + 7919 * rank).astype(np.int32))
+        gb = [torch.empty_like(b_r) for _ in range(ws)]
+        dist.all_gather(gb, b_r)
+        assert not torch.equal(gb[0], gb[1])
+
+        # --impl reference: rank 0 alone runs and prints; other ranks exit without work
+        if rank != 0:
+            out = io.StringIO()
+            with redirect_stdout(out):
+                bench.main(["--impl", "reference", "--gpus", str(ws), "--steps", "1", "--warmup", "3"])
+            assert out.getvalue() == ""
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # report to the parent instead of hanging it
+        q.put((rank, repr(e)))
+
+
+def test_two_rank_gloo_host_logic():
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+    assert results == {0: "ok", 1: "ok"}, results
