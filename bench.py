@@ -164,20 +164,29 @@ class Layer:
         self.A = synth.gaussian_device((w["R"], w["K"]), 0.02, synth.F16, sa, device)
         self.B = synth.gaussian_device((w["K"], w["T"]), 1.0, synth.F16, sb + 7919 * rank, device)
         self.bias = synth.gaussian_device((w["R"],), 0.5, synth.F16, sb + 1, device)
-        self.x = venom.compress(self.A, V=w["V"], M=w["M"], check=True)
         # execution form of the operand: the V:N:M arrays themselves, or the same matrix re-encoded
-        # as V:2:4 (dense-K, reading #18) when that runs faster on B200
+        # as V:2:4 (reading #18) when that runs faster on B200; either way with the
+        # metadata in tensor-core order
         self.expand = (form == "2to4") or (form == "auto" and venom.prefers_2to4(w["R"], w["K"], w["T"], w["V"], w["M"]))
-        self.y = venom.expand_2to4(self.x, check=True) if self.expand else self.x
+        if self.expand:
+            self.x, self.y = venom.compress_2to4(self.A, V=w["V"], M=w["M"], check=True)
+        else:
+            self.x = venom.compress(self.A, V=w["V"], M=w["M"], check=True)
+            self.y = venom.order_metadata(self.x)
         self.C = torch.empty((w["R"], w["T"]), dtype=torch.float16, device=device)
         self.D = torch.empty((w["R"], w["K"]), dtype=torch.float16, device=device)
         self.flops = useful_flops(w)
 
     def compress(self, A=None):
+        """a1-a3 (+ the execution form): one fused kernel for the V:2:4 form, else compress +
+        tensor-core ordering of the metadata."""
         w = self.w
-        self.venom.compress(self.A if A is None else A, V=w["V"], M=w["M"], out=self.x)  # a1-a3
+        A = self.A if A is None else A
         if self.expand:
-            self.venom.expand_2to4(self.x, out=self.y)
+            self.venom.compress_2to4(A, V=w["V"], M=w["M"], out=(self.x, self.y))
+        else:
+            self.venom.compress(A, V=w["V"], M=w["M"], out=self.x)
+            self.venom.order_metadata(self.y)
 
     def spmm(self, B=None, out=None, **kw):
         return self.venom.spmm(self.y, self.B if B is None else B, bias=self.bias,
@@ -224,7 +233,8 @@ def run_gpu(args, ws, rank, local):
             if part_events is not None:
                 part_events[3].record(stream)
 
-    launches_per_step = sum((3 if args.step == "full" else 2) + int(L.expand) for L in layers)
+    # [compress_2to4 | compress + order_metadata] + spmm (+ decompress) per layer
+    launches_per_step = sum((1 if L.expand else 2) + 1 + int(args.step == "full") for L in layers)
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -343,9 +353,10 @@ def run_gpu(args, ws, rank, local):
             "data": "synthetic (seeded; A ~ N(0,0.02^2), B ~ N(0,1), fp16)",
             "config": {"workload": args.workload, "layers": [L.name for L in layers],
                        "V:N:M": f"{w0['V']}:2:{w0['M']}", "tokens_per_gpu": w0["T"],
-                       "step": ("compress+spmm+decompress per layer" if args.step == "full" else "spmm per layer"),
-                       "operand_form": ["V:2:4 re-encoded (expand inside the step)" if L.expand else "V:N:M"
-                                        for L in layers],
+                       "step": ("compress(+execution form)+spmm" + ("+decompress" if args.step == "full" else "")
+                                + " per layer"),
+                       "operand_form": ["V:2:4 re-encoding, fused into compress (venom_compress_2to4)" if L.expand
+                                        else "V:N:M (+ venom_order_metadata)" for L in layers],
                        "l2": "flushed (512 MiB write) before every timed step", "parallelism": f"T-split x{ws}"},
             "spmm_only": {"tflops": round(achieved, 3), "ms_per_launch": [round(x, 5) for x in per_launch_ms]},
             "step_breakdown_ms": {"compress_all_layers": round(compress_ms, 5),

@@ -107,6 +107,8 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0
  *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
  *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
+ * metadata may be NULL when opts->metadata_tc is given; column_idx may be NULL when M == 4 (it is the
+ * identity and never read).
  * Metadata validity is NOT checked here (use venom_decompress with dev_status to validate);
  * malformed metadata gives undefined values, never out-of-bounds accesses.
  */
@@ -136,9 +138,27 @@ venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,
                                 int32_t* dev_status, venom_stream_t stream);
 
 /*
+ * Fused compression + execution-form preparation (one pass over A): writes everything
+ * venom_compress writes (values, metadata, column_idx: the canonical V:N:M arrays, bit-identical to
+ * venom_compress) and, for the same matrix, the V:2:4 re-encoding's values (as venom_expand_2to4:
+ * values_2to4 dtype[R][K/4][2]) and its metadata in tensor-core order (as venom_order_metadata on
+ * the re-encoding: metadata_2to4_tc, venom_metadata_tc_bytes(R, K, {v, 2, 4}) bytes). The pair
+ * (values_2to4, metadata_2to4_tc) is a complete venom_spmm operand of format {v, 2, 4}: pass it with
+ * opts.metadata_tc and NULL metadata / column_idx. Requires M % 8 == 0, M | 128, V % 16 == 0,
+ * V <= 256, K % 16 == 0 (else VENOM_ERR_UNSUPPORTED_PATTERN); values_2to4 / metadata_2to4_tc
+ * 16-byte aligned. Non-finite inputs are reported through *dev_status like venom_compress.
+ */
+venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t lda,
+                                  venom_dtype_t dt, venom_format_t f,
+                                  void* values, uint8_t* metadata, uint8_t* column_idx,
+                                  void* values_2to4, uint8_t* metadata_2to4_tc,
+                                  int32_t* dev_status, venom_stream_t stream);
+
+/*
  * Planner hint: 1 when venom_spmm over venom_expand_2to4's output is expected to run faster on
- * B200 than venom_spmm on the V:N:M operand itself for this shape (R, K, T, f); 0 otherwise,
- * including for any invalid format. Pure host function, no device access.
+ * B200 than venom_spmm on the V:N:M operand itself for this shape (R, K, T, f), and the fused
+ * venom_compress_2to4 applies; 0 otherwise, including for any invalid format. Pure host function,
+ * no device access.
  */
 int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f);
 
@@ -156,8 +176,12 @@ typedef struct {
   int32_t stages;
   int32_t max_ctas;
   int32_t strategy;
-  int32_t cta_pair;  /* dense-K only: 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2,
-                        256-row tiles, B split between the pair's shared memories); 0 = default 2 */
+  int32_t cta_pair;  /* 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2, 256-row tiles,
+                        B split between the pair's shared memories); 0 = library default */
+  const uint8_t* metadata_tc;  /* nullable DEVICE pointer: the operand's metadata in tensor-core
+                        order (venom_order_metadata). When set, the gathered kernel loads it with
+                        TMA and copies it to TMEM with tcgen05.cp instead of permuting `metadata`
+                        on the fly; `metadata` is then not read. Must be 16-byte aligned. */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
@@ -166,6 +190,22 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
                              void* C, int64_t ldc, const void* bias,
                              venom_dtype_t dt, const venom_spmm_opts_t* opts,
                              venom_stream_t stream);
+
+/*
+ * Tensor-core order of the metadata — the paper's "storage order" idea (§4.1:
+ * m-indices are stored in the order the hardware consumes them) re-targeted to tcgen05: the same
+ * nibbles as `metadata`, permuted so that the block for one 128-row tile and one k-stage of 32
+ * groups is the 2 KB TMEM image the sparse MMA reads. Layout:
+ * uint32[ceil(R/128)][ceil(G/32)][128 lanes][4 MMAs], G = K/M; lane L, MMA kb holds the 16 bits of
+ * groups 32·ks + 8·kb + 4·((L>>3)&1) .. +3 of row (L&7) + 16·(L>>4) (low half) and of that row + 8
+ * (high half); rows >= R and groups >= G are filled with the zero-value code 0x4 (m-indices 0,1).
+ * venom_metadata_tc_bytes returns the size in bytes (-1 for an invalid format). Requires G % 4 == 0
+ * (VENOM_ERR_UNSUPPORTED_PATTERN otherwise). metadata_tc: caller-owned device buffer, 16-byte
+ * aligned. Metadata validity is not checked (use venom_decompress with dev_status).
+ */
+int64_t venom_metadata_tc_bytes(int64_t R, int64_t K, venom_format_t f);
+venom_status_t venom_order_metadata(const uint8_t* metadata, int64_t R, int64_t K, venom_format_t f,
+                                    uint8_t* metadata_tc, venom_stream_t stream);
 
 /* Number of kernels venom_spmm / venom_compress / venom_decompress launch per call (1 each). */
 int32_t venom_kernels_per_call(void);

@@ -30,7 +30,9 @@ STATUS_NAMES = {
     8: "VENOM_ERR_ARCH", 9: "VENOM_ERR_CUDA",
 }
 EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
-            "venom_spmm_ex", "venom_expand_2to4", "venom_prefer_2to4", "venom_kernels_per_call", "venom_status_string",
+            "venom_spmm_ex", "venom_expand_2to4", "venom_compress_2to4", "venom_prefer_2to4",
+            "venom_metadata_tc_bytes",
+            "venom_order_metadata", "venom_kernels_per_call", "venom_status_string",
             "venom_version"]
 
 
@@ -46,7 +48,8 @@ class _Format(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
-                ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32)]
+                ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
+                ("metadata_tc", ctypes.c_void_p)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -70,11 +73,15 @@ def lib() -> ctypes.CDLL:
         L.venom_spmm.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int, P]
         L.venom_expand_2to4.argtypes = [P, P, P, I64, I64, ctypes.c_int, _Format, P, P, P, P, P]
         L.venom_prefer_2to4.argtypes = [I64, I64, I64, _Format]
+        L.venom_metadata_tc_bytes.argtypes = [I64, I64, _Format]
+        L.venom_metadata_tc_bytes.restype = I64
+        L.venom_order_metadata.argtypes = [P, I64, I64, _Format, P, P]
+        L.venom_compress_2to4.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P, P, P]
         L.venom_prefer_2to4.restype = ctypes.c_int
         L.venom_spmm_ex.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int,
                                     ctypes.POINTER(_Opts), P]
         for fn in ("venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
-                   "venom_spmm_ex", "venom_expand_2to4"):
+                   "venom_spmm_ex", "venom_expand_2to4", "venom_order_metadata", "venom_compress_2to4"):
             getattr(L, fn).restype = ctypes.c_int
         L.venom_status_string.argtypes = [ctypes.c_int]
         L.venom_status_string.restype = ctypes.c_char_p
@@ -117,6 +124,7 @@ class VNMTensor:
     V: int
     M: int
     N: int = 2
+    metadata_tc: Optional[torch.Tensor] = None  # uint8, tensor-core order (order_metadata)
 
     @property
     def dtype(self) -> torch.dtype:
@@ -188,9 +196,11 @@ def decompress(x: VNMTensor, out: Optional[torch.Tensor] = None, status: Optiona
 
 def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
-         max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0) -> torch.Tensor:
+         max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0,
+         use_metadata_tc: bool = True) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
-    B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T]."""
+    B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T]. When x carries
+    tensor-core-ordered metadata (order_metadata) it is used unless use_metadata_tc is False."""
     assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[0] == x.K
     assert B.dtype == x.dtype
     T = B.shape[1]
@@ -199,15 +209,70 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     assert out.stride(1) == 1 and out.shape == (x.R, T)
     if bias is not None:
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
-    opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair)
-    st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
-                             ctypes.c_void_p(x.column_idx.data_ptr()), x.R, x.K, x.fmt(),
+    mtc = x.metadata_tc.data_ptr() if (use_metadata_tc and x.metadata_tc is not None) else None
+    opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc)
+    st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
+                             ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
+                             ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),
+                             x.R, x.K, x.fmt(),
                              ctypes.c_void_p(B.data_ptr()), T, B.stride(0),
                              ctypes.c_void_p(out.data_ptr()), out.stride(0),
                              ctypes.c_void_p(bias.data_ptr() if bias is not None else 0),
                              _dt(x.dtype), ctypes.byref(opts), _stream(B.device))
     _check(st, "venom_spmm")
     return out
+
+
+def compress_2to4(A: torch.Tensor, V: int, M: int, status: Optional[torch.Tensor] = None,
+                  check: bool = False, out=None):
+    """Fused compress + V:2:4 execution form (venom_compress_2to4): returns (x, y) where x is the
+    canonical V:N:M operand (== compress(A)) and y the same matrix as V:2:4 with tensor-core-ordered
+    metadata (y.metadata / y.column_idx are empty: spmm does not read them)."""
+    assert A.is_cuda and A.dim() == 2 and A.stride(1) == 1
+    R, K = A.shape
+    dev = A.device
+    if out is None:
+        x = VNMTensor(torch.empty((R, K // M, 2), dtype=A.dtype, device=dev),
+                      torch.empty((R, (K // M + 1) // 2), dtype=torch.uint8, device=dev),
+                      torch.empty((R // V, K // M, 4), dtype=torch.uint8, device=dev), R, K, V, M)
+        y = VNMTensor(torch.empty((R, K // 4, 2), dtype=A.dtype, device=dev),
+                      torch.empty(0, dtype=torch.uint8, device=dev), torch.empty(0, dtype=torch.uint8, device=dev),
+                      R, K, V, 4, metadata_tc=torch.empty(max(metadata_tc_bytes(R, K, V, 4), 16),
+                                                          dtype=torch.uint8, device=dev))
+    else:
+        x, y = out
+    if check and status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = lib().venom_compress_2to4(ctypes.c_void_p(A.data_ptr()), R, K, A.stride(0), _dt(A.dtype), _Format(V, 2, M),
+                                   ctypes.c_void_p(x.values.data_ptr()), ctypes.c_void_p(x.metadata.data_ptr()),
+                                   ctypes.c_void_p(x.column_idx.data_ptr()), ctypes.c_void_p(y.values.data_ptr()),
+                                   ctypes.c_void_p(y.metadata_tc.data_ptr()),
+                                   ctypes.c_void_p(status.data_ptr() if status is not None else 0), _stream(dev))
+    _check(st, "venom_compress_2to4")
+    if check:
+        _check(int(status.item()), "venom_compress_2to4 (device status)")
+    return x, y
+
+
+def metadata_tc_bytes(R: int, K: int, V: int, M: int) -> int:
+    n = lib().venom_metadata_tc_bytes(R, K, _Format(V, 2, M))
+    if n < 0:
+        raise VenomError(4, "venom_metadata_tc_bytes")
+    return n
+
+
+def order_metadata(x: VNMTensor, out: Optional[torch.Tensor] = None) -> VNMTensor:
+    """Attach the metadata in tensor-core order (the paper's storage-order idea)
+    to x, in place; spmm then loads it with TMA instead of permuting metadata on the fly."""
+    n = metadata_tc_bytes(x.R, x.K, x.V, x.M)
+    if out is None:
+        out = x.metadata_tc if (x.metadata_tc is not None and x.metadata_tc.numel() == n) else \
+            torch.empty(max(n, 16), dtype=torch.uint8, device=x.metadata.device)
+    st = lib().venom_order_metadata(ctypes.c_void_p(x.metadata.data_ptr()), x.R, x.K, x.fmt(),
+                                    ctypes.c_void_p(out.data_ptr()), _stream(x.metadata.device))
+    _check(st, "venom_order_metadata")
+    x.metadata_tc = out
+    return x
 
 
 def expand_2to4(x: VNMTensor, out: Optional[VNMTensor] = None, status: Optional[torch.Tensor] = None,

@@ -208,6 +208,242 @@ __global__ void __launch_bounds__(256) vnm_compress_kernel(
   }
 }
 
+// Compression, shared-memory tile variant (the default when V·W·2 bytes fit): the CTA's V × W
+// block of A (W = gpc·M columns) is read from HBM exactly once with 16-byte loads, all in flight
+// together, then the three phases of vnm_compress_kernel run on the shared-memory copy:
+//   phase 1: thread per column, fp64 sum of |a| over the V rows in ascending order (the oracle's
+//            order; exact for fp16, so bit-identical scores — DESIGN.md reading #2);
+//   phase 2: thread per group: top-4 columns by (score desc, index asc), stored ascending;
+//   phase 3: thread per (row, pair of groups): top-2 of the 4 by (|a| desc, position asc), raw-bit
+//            value copy, nibble packing.
+template <bool kBF16, bool kExpand>
+__global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
+    const uint16_t* __restrict__ A, int64_t R, int64_t K, int64_t lda, int V, int M, int64_t G,
+    int gpc, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
+    uint8_t* __restrict__ column_idx, int32_t* __restrict__ status,
+    uint32_t* __restrict__ values2, uint32_t* __restrict__ meta_tc, int dbg) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int64_t rb = blockIdx.y;
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * gpc;
+  const int ng = static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
+  const int W = gpc * M;                 // tile pitch (elements)
+  const int ncols = ng * M;
+  const int64_t k0 = g0 * M;
+  const int64_t row0 = rb * V;
+  const int64_t meta_row = (G + 1) / 2;
+  uint16_t* tile = reinterpret_cast<uint16_t*>(smem_raw);                        // [V][W]
+  double* s_score = reinterpret_cast<double*>(smem_raw + ((static_cast<size_t>(V) * W * 2 + 15) & ~size_t(15)));
+  uint32_t* s_sel = reinterpret_cast<uint32_t*>(s_score + W);                    // [gpc]
+  // kExpand: the V:2:4 re-encoding's nibbles of this tile, [V][W/8] bytes (subgroups 2j, 2j+1)
+  uint8_t* s_m2 = reinterpret_cast<uint8_t*>(s_sel + gpc);
+
+  // ---- phase 0: the block tile, 16-byte loads (8 columns) where aligned, else element-wise
+  bool bad = false;
+  const int nvec = ncols / 8;  // full 8-column vectors of a row (W % 8 == 0 by construction)
+  const bool vec_ok = ((lda & 7) == 0) && ((k0 & 7) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  if (vec_ok && !(dbg & 1)) {
+    for (int t = threadIdx.x; t < V * nvec; t += blockDim.x) {
+      const int i = t / nvec, cv = t - i * nvec;
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(A + (row0 + i) * lda + k0) + cv);
+      *reinterpret_cast<uint4*>(tile + i * W + 8 * cv) = w;
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        bad |= bits_non_finite<kBF16>(static_cast<uint16_t>((ww[u >> 1] >> (16 * (u & 1))) & 0xFFFFu));
+    }
+  }
+  const int cstart = vec_ok ? 8 * nvec : 0;
+  const int ntail = ncols - cstart;
+  if (ntail > 0) {
+    for (int t = threadIdx.x; t < V * ntail; t += blockDim.x) {
+      const int i = t / ntail, c = cstart + (t - i * ntail);
+      const uint16_t b = __ldg(A + (row0 + i) * lda + k0 + c);
+      tile[i * W + c] = b;
+      bad |= bits_non_finite<kBF16>(b);
+    }
+  }
+  if (bad && status != nullptr) atomicMax(status, kStatusNonFinite);
+  __syncthreads();
+
+  // ---- phase 1: column L1 mass, fp64, ascending rows
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+    double acc = 0.0;
+    if (dbg & 2) {
+    } else if constexpr (!kBF16) {
+      // fp16: |a| = k·2^-24 with integer k < 2^40, so the column sum is an exact integer (< 2^53
+      // for V <= 8192): accumulate k in 64-bit integers (any order, 4 independent chains) and
+      // convert once — the same value as the oracle's sequential fp64 sum (reading #2)
+      uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      auto kval = [](uint16_t bb) -> uint64_t {
+        const uint32_t e = (bb >> 10) & 0x1Fu, f = bb & 0x3FFu;
+        return e == 0 ? static_cast<uint64_t>(f) : (static_cast<uint64_t>(1024u + f) << (e - 1));
+      };
+      int i = 0;
+      for (; i + 4 <= V; i += 4) {
+        s0 += kval(tile[(i + 0) * W + c]);
+        s1 += kval(tile[(i + 1) * W + c]);
+        s2 += kval(tile[(i + 2) * W + c]);
+        s3 += kval(tile[(i + 3) * W + c]);
+      }
+      for (; i < V; ++i) s0 += kval(tile[i * W + c]);
+      acc = ldexp(static_cast<double>(s0 + s1 + s2 + s3), -24);
+    } else {
+      // bf16: not exact in general — the oracle's order (ascending rows, fp64)
+      for (int i = 0; i < V; ++i) acc = __dadd_rn(acc, static_cast<double>(fabsf(bits_to_float<kBF16>(tile[i * W + c]))));
+    }
+    s_score[c] = acc;
+  }
+  __syncthreads();
+
+  // ---- phase 2: the four most significant columns of each block
+  for (int q = threadIdx.x; q < ng; q += blockDim.x) {
+    const double* sc = s_score + q * M;
+    int c[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int best = -1;
+      double bs = 0.0;
+      for (int j = 0; j < M; ++j) {
+        bool taken = false;
+#pragma unroll
+        for (int u = 0; u < t; ++u) taken |= (c[u] == j);
+        if (taken) continue;
+        if (best < 0 || sc[j] > bs) {
+          best = j;
+          bs = sc[j];
+        }
+      }
+      c[t] = best;
+    }
+#define VENOM_CSWAP(x, y) \
+  if (c[x] > c[y]) {      \
+    int t_ = c[x];        \
+    c[x] = c[y];          \
+    c[y] = t_;            \
+  }
+    VENOM_CSWAP(0, 1) VENOM_CSWAP(2, 3) VENOM_CSWAP(0, 2) VENOM_CSWAP(1, 3) VENOM_CSWAP(1, 2)
+#undef VENOM_CSWAP
+    const uint32_t word = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) |
+                          (static_cast<uint32_t>(c[2]) << 16) | (static_cast<uint32_t>(c[3]) << 24);
+    reinterpret_cast<uint32_t*>(column_idx)[rb * G + g0 + q] = word;
+    s_sel[q] = word;
+  }
+  __syncthreads();
+
+  // ---- phase 3: thread per (row, group): the two largest |w| among the selected columns (2:4);
+  // consecutive threads take consecutive groups of a row (coalesced value stores), the two
+  // nibbles of a metadata byte are joined with a lane shuffle
+  const int per_row = ng + (ng & 1);  // even: lane pairs (2j, 2j+1) share a metadata byte
+  const int work3 = (dbg & 4) ? 0 : V * per_row;
+  for (int w0 = 0; w0 < work3; w0 += blockDim.x) {
+    const int w = w0 + static_cast<int>(threadIdx.x);
+    const bool act = w < work3;
+    const int i = act ? w / per_row : 0;
+    const int q = act ? w - i * per_row : 0;
+    const bool live = act && q < ng;
+    const int64_t row = row0 + i;
+    uint32_t nibble = 0;
+    if (live) {
+      const uint32_t cw = s_sel[q];
+      const uint16_t* trow = tile + i * W + q * M;
+      uint16_t v[4];
+      uint32_t mag[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        v[t] = trow[(cw >> (8 * t)) & 0xFFu];
+        mag[t] = v[t] & 0x7FFFu;  // |w| order for finite sign-magnitude formats; ±0 tie
+      }
+      int p0 = 0;
+#pragma unroll
+      for (int t = 1; t < 4; ++t)
+        if (mag[t] > mag[p0]) p0 = t;
+      int p1 = -1;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t != p0 && (p1 < 0 || mag[t] > mag[p1])) p1 = t;
+      const int lo = min(p0, p1), hi = max(p0, p1);
+      nibble = static_cast<uint32_t>(lo | (hi << 2));
+      reinterpret_cast<uint32_t*>(values)[row * G + g0 + q] =
+          static_cast<uint32_t>(v[lo]) | (static_cast<uint32_t>(v[hi]) << 16);
+      if constexpr (kExpand) {
+        // the same matrix as V:2:4 over the original K (reading #18): per 4-column
+        // subgroup the kept values (inserted zeros +0.0) and one nibble; M % 8 == 0, so the
+        // group's subgroups fill whole bytes of s_m2
+        const int ca = static_cast<int>((cw >> (8 * lo)) & 0xFFu), cb = static_cast<int>((cw >> (8 * hi)) & 0xFFu);
+        const int sub = M / 4;
+        uint32_t* v2 = values2 + row * (K / 4) + (g0 + q) * sub;
+        uint32_t nbits = 0;
+        for (int u = 0; u < sub; ++u) {
+          const int j0 = 4 * u;
+          const bool in0 = (ca >= j0 && ca < j0 + 4), in1 = (cb >= j0 && cb < j0 + 4);
+          uint32_t wv, nb;
+          if (in0 && in1) {
+            wv = static_cast<uint32_t>(v[lo]) | (static_cast<uint32_t>(v[hi]) << 16);
+            nb = static_cast<uint32_t>(ca - j0) | (static_cast<uint32_t>(cb - j0) << 2);
+          } else if (in0 || in1) {
+            const uint32_t x = in0 ? v[lo] : v[hi];
+            const uint32_t ii = static_cast<uint32_t>((in0 ? ca : cb) - j0);
+            wv = (ii == 0u) ? x : (x << 16);
+            nb = (ii == 0u) ? 0x4u : (ii << 2);
+          } else {
+            wv = 0u;
+            nb = 0x4u;
+          }
+          v2[u] = wv;
+          nbits |= nb << (4 * (u & 1));
+          if (u & 1) {
+            s_m2[i * (W / 8) + (q * sub + u) / 2] = static_cast<uint8_t>(nbits);
+            nbits = 0;
+          }
+        }
+      }
+    }
+    // join the nibbles of groups (2j, 2j+1): per_row is even, so partners are adjacent lanes
+    const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, nibble, 1);
+    if (live && (q & 1) == 0) {
+      const uint32_t byte = nibble | ((q + 1 < ng ? other : 0u) << 4);
+      metadata[row * meta_row + (g0 + q) / 2] = static_cast<uint8_t>(byte);
+    }
+  }
+
+  if constexpr (kExpand) {
+    // ---- phase 4: tensor-core order of the re-encoded metadata (venom_order_metadata's layout)
+    // for the 128-row-tile lanes whose rows this CTA owns, over its k-stages of 32 subgroups
+    // (W % 128 == 0 and g0·M % 128 == 0: the CTA owns whole k-stages). Rows >= R of the last
+    // row tile and subgroups >= K/4 read as 0x4 nibbles.
+    __syncthreads();
+    const int64_t G2 = K / 4;
+    const int64_t num_ks2 = (G2 + 31) / 32;
+    const int64_t ks0 = (g0 * M / 4) / 32;
+    const int nks = W / 128;
+    const int64_t r1 = (row0 + V == R) ? ((R + 127) / 128) * 128 : row0 + V;  // rows covered
+    const int nrows16 = static_cast<int>((r1 - row0) / 16);                    // 16-row bands
+    // one work item = (k-stage, 16-row band, lane-in-band b in [0,8) x {k1}, kb): the band's 16 lanes
+    const int items = nks * nrows16 * 16 * 4;
+    for (int t = threadIdx.x; t < ((dbg & 8) ? 0 : items); t += blockDim.x) {
+      const int kb = t & 3;
+      const int l16 = (t >> 2) & 15;  // lane within the band: L & 15 = (L & 7) | (k1 << 3)
+      const int rest = t >> 6;
+      const int band = rest % nrows16;
+      const int ksl = rest / nrows16;
+      const int64_t ks = ks0 + ksl;
+      if (ks >= num_ks2) continue;
+      const int64_t ra = row0 + 16 * band + (l16 & 7);
+      const int k1 = l16 >> 3;
+      const int64_t mt = ra / 128;
+      const int L = static_cast<int>(((ra % 128) / 16) * 16) + l16;
+      const int e0 = ksl * 32 + kb * 8 + 4 * k1;  // first subgroup (tile-relative)
+      uint32_t lo = 0x4444u, hi = 0x4444u;
+      if (ks * 32 + kb * 8 + 4 * k1 < G2) {
+        const int ia = static_cast<int>(ra - row0);
+        if (ra < R) lo = s_m2[ia * (W / 8) + e0 / 2] | (static_cast<uint32_t>(s_m2[ia * (W / 8) + e0 / 2 + 1]) << 8);
+        if (ra + 8 < R) hi = s_m2[(ia + 8) * (W / 8) + e0 / 2] | (static_cast<uint32_t>(s_m2[(ia + 8) * (W / 8) + e0 / 2 + 1]) << 8);
+      }
+      meta_tc[((mt * num_ks2 + ks) * 128 + L) * 4 + kb] = lo | (hi << 16);
+    }
+  }
+}
+
 // Decompression: grid (column chunks, rows); thread per (row, kVec consecutive output elements).
 // Output +0.0 except the kept positions. Validates metadata when `status` is non-null. 32-bit
 // index arithmetic inside a row (K < 2^31), group/position advanced incrementally.
@@ -218,10 +454,13 @@ __global__ void __launch_bounds__(256) vnm_decompress_kernel(
     uint16_t* __restrict__ out, int64_t lda, int32_t* __restrict__ status) {
   const int64_t meta_row = (G + 1) / 2;
   const int kk = static_cast<int>(K);
-  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * kVec;
-  if (k0 >= kk) return;
+  const int chunks = static_cast<int>((K + kVec - 1) / kVec);
+  const int total = static_cast<int>(R * chunks);  // host guarantees < 2^31
   bool bad = false;
-  for (int64_t row = blockIdx.y; row < R; row += gridDim.y) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int rowi = idx / chunks;
+    const int64_t row = rowi;
+    const int k0 = (idx - rowi * chunks) * kVec;
     const int64_t rb = row / V;
     const uint32_t* cw_row = reinterpret_cast<const uint32_t*>(column_idx) + rb * G;
     const uint32_t* v_row = reinterpret_cast<const uint32_t*>(values) + row * G;
@@ -273,6 +512,44 @@ __global__ void __launch_bounds__(256) vnm_decompress_kernel(
   if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
 }
 
+// Decompression fast path for M % 8 == 0 (16-byte output vectors never straddle a group):
+// grid (chunk blocks, row slots); thread per (row, 8 outputs); the two kept positions are placed
+// with shifts, no per-element branches. CPG = M / 8 when it is a compile-time 1, 2 or 4, else 0
+// (runtime M).
+template <int CPG>
+__global__ void __launch_bounds__(256) vnm_decompress_m8_kernel(
+    const uint32_t* __restrict__ values, const uint8_t* __restrict__ metadata,
+    const uint32_t* __restrict__ column_idx, int R, int K, int V, int M, int G,
+    uint16_t* __restrict__ out, int64_t lda, int32_t* __restrict__ status) {
+  const int chunks = K / 8;
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= chunks) return;
+  const int meta_row = (G + 1) / 2;
+  const int cpg = CPG ? CPG : M / 8;  // 8-output chunks per group
+  const int g = ch / cpg;
+  const int j0 = (ch - g * cpg) * 8;  // first column of this chunk within the group
+  bool bad = false;
+  for (int row = blockIdx.y; row < R; row += gridDim.y) {
+    const uint32_t cw = __ldg(column_idx + (row / V) * G + g);
+    const uint32_t nib = (__ldg(metadata + static_cast<int64_t>(row) * meta_row + (g >> 1)) >> (4 * (g & 1))) & 0xFu;
+    const uint32_t vv = __ldg(values + static_cast<int64_t>(row) * G + g);
+    const uint32_t p0 = nib & 3u, p1 = nib >> 2;
+    bad |= !((cw & 0xFFu) < ((cw >> 8) & 0xFFu) && ((cw >> 8) & 0xFFu) < ((cw >> 16) & 0xFFu) &&
+             ((cw >> 16) & 0xFFu) < (cw >> 24) && (cw >> 24) < static_cast<uint32_t>(M)) ||
+           !(p0 < p1);
+    const int d0 = static_cast<int>((cw >> (8 * p0)) & 0xFFu) - j0;  // offsets inside the chunk
+    const int d1 = static_cast<int>((cw >> (8 * p1)) & 0xFFu) - j0;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if ((d0 >> 1) == q) w[q] |= (vv & 0xFFFFu) << (16 * (d0 & 1));
+      if ((d1 >> 1) == q) w[q] |= (vv >> 16) << (16 * (d1 & 1));
+    }
+    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * lda + 8 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
+}
+
 // Re-encoding V:N:M (M % 4 == 0) -> V:2:4 over the original K (reading #18; the oracle's
 // oracle_expand_2to4 states the rules). grid (pairs of groups, rows); thread per (row, 2 groups):
 // the kept positions of each group are resolved through column_idx and the m-indices, and every
@@ -282,14 +559,16 @@ __global__ void __launch_bounds__(256) vnm_expand_2to4_kernel(
     const uint32_t* __restrict__ column_idx, int64_t R, int V, int M, int64_t G,
     uint32_t* __restrict__ values2, uint8_t* __restrict__ metadata2,
     uint32_t* __restrict__ column_idx2, int32_t* __restrict__ status) {
-  const int64_t npairs = (G + 1) / 2;
-  const int64_t pp = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (pp >= npairs) return;
+  const int npairs = static_cast<int>((G + 1) / 2);
+  const int total = static_cast<int>(R * npairs);  // host guarantees < 2^31
   const int sub = M / 4;                       // subgroups per group
   const int64_t G2 = G * sub, meta_row = (G + 1) / 2, meta_row2 = (G2 + 1) / 2;
   bool bad = false;
-  for (int64_t row = blockIdx.y; row < R; row += gridDim.y) {
-    const int64_t rb = row / V;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int rowi = idx / npairs;
+    const int64_t row = rowi;
+    const int64_t pp = idx - rowi * npairs;
+    const int64_t rb = rowi / V;
     uint32_t acc = 0;   // pending nibbles of the current output byte
     for (int h = 0; h < 2; ++h) {
       const int64_t g = 2 * pp + h;
@@ -331,6 +610,37 @@ __global__ void __launch_bounds__(256) vnm_expand_2to4_kernel(
     }
   }
   if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
+}
+
+// Tensor-core order of the metadata (DESIGN.md §5 "prepared metadata"): the canonical nibbles
+// permuted into the TMEM layout tcgen05.mma.sp reads, one 2 KB block per (128-row tile mt, k-stage
+// ks of 32 groups): u32 out[mt][ks][L][kb] for lane L = 0..127 and K = 32 MMA kb = 0..3 holds the 16
+// bits of groups ks·32 + kb·8 + 4·k1 .. +3 (k1 = (L >> 3) & 1) for row (L & 7) + 16·(L >> 4) in its
+// low half and for that row + 8 in its high half. Rows >= R and groups >= G read as 0x4 nibbles
+// (m-indices {0,1} of all-zero values). Thread per (mt, ks, L): one 16-byte store.
+__global__ void __launch_bounds__(256) vnm_order_metadata_kernel(const uint8_t* __restrict__ metadata,
+                                                                 int64_t R, int64_t G,
+                                                                 int64_t num_ks, int64_t total,
+                                                                 uint32_t* __restrict__ out) {
+  // thread per output word: idx = ((mt·num_ks + ks)·128 + L)·4 + kb; metadata rows are G/2 bytes
+  // (G % 4 == 0), so every 4-group chunk is one aligned 16-bit word
+  const int64_t meta_row2 = G / 4;  // 16-bit words per metadata row
+  const uint16_t* m16 = reinterpret_cast<const uint16_t*>(metadata);
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int kb = static_cast<int>(idx & 3);
+    const int L = static_cast<int>((idx >> 2) & 127);
+    const int64_t blk = idx >> 9;  // mt * num_ks + ks
+    const int64_t ks = blk % num_ks, mt = blk / num_ks;
+    const int64_t ra = mt * 128 + (L & 7) + 16 * (L >> 4), rb = ra + 8;
+    const int64_t w16 = ks * 8 + kb * 2 + ((L >> 3) & 1);  // 16-bit word of groups 4·w16 .. +3
+    uint32_t lo = 0x4444u, hi = 0x4444u;
+    if (w16 < meta_row2) {
+      if (ra < R) lo = __ldg(m16 + ra * meta_row2 + w16);
+      if (rb < R) hi = __ldg(m16 + rb * meta_row2 + w16);
+    }
+    out[idx] = lo | (hi << 16);
+  }
 }
 
 }  // namespace venom

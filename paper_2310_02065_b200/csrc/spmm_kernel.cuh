@@ -15,9 +15,10 @@
 //             issue is serial per warp (~70 cycles per op, tools/microbench.cu), so P warps issue;
 //   * warp P  MMA: tcgen05.cp metadata SMEM->TMEM, tcgen05.mma.sp (M=128, N=BN, K=32) with fp32
 //             accumulation in TMEM (the paper's stage 2 on 5th-gen sparse tensor cores);
-//   * warps P+1..P+4 epilogue: tcgen05.ld -> +bias -> round -> 16-byte global stores (stage 3),
-//             overlapped with the next tile's main loop when TMEM allows two accumulators;
-//   * warps P+5..P+8 metadata: canonical per-row nibbles -> the tensor-core metadata layout in
+//   * warps P+1..P+8 epilogue: tcgen05.ld -> +bias -> round into registers, release the
+//             accumulator, then 16-byte global stores (stage 3) overlapping the next tile;
+//   * warps P+9..P+12 metadata (only without pre-ordered metadata): canonical per-row nibbles ->
+//             the tensor-core metadata layout in
 //             SMEM ("we also load directly ... the m-indices"), prefetched ahead.
 // V = 128·k uses one V-block per tile; V ∈ {32, 64} packs NB = 128/V blocks into one 128-row A
 // tile and issues one MMA per block (each block has its own gathered B' and accumulator).
@@ -48,8 +49,10 @@ struct SpmmParams {
   int dbg;  // debug/ablation flags (0 in production)
 };
 
-template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8, int CG_ = 1>
+template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8, int CG_ = 1, bool PRE_ = false>
 struct SpmmCfg {
+  static constexpr bool PRE = PRE_;           // metadata pre-ordered for the tensor core (TMA-loaded,
+                                              // tcgen05.cp to TMEM by the MMA thread): no metadata warps
   static constexpr int NB = NB_;              // V-blocks per 128-row tile
   static constexpr int CG = CG_;              // 2: CTA pair (cta_group::2, 256-row tiles): needs
                                               // one column_idx per pair tile (V % 256 == 0 or M == 4)
@@ -62,8 +65,9 @@ struct SpmmCfg {
   static constexpr int A_BYTES = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
   static constexpr int B_CHUNK = 128 * 128;   // 128 K'-rows × 64 columns × 2 B (SW128, MN-major)
   static constexpr int B_BYTES = (BNH / 64) * B_CHUNK;
-  static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES;
-  static constexpr int TX_BYTES = A_BYTES + NB * B_BYTES;  // per CTA
+  static constexpr int E_BYTES = PRE_ ? 128 * 16 : 0;  // 128 lanes × 4 metadata words
+  static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES + E_BYTES;
+  static constexpr int TX_BYTES = STAGE_BYTES;  // per CTA
   static constexpr int ACC_COLS = NB * BN;
   // TMEM: accumulators, then 4 metadata columns per stage (written by tcgen05.st)
   static constexpr int ACC_BUFS = (2 * ACC_COLS + 4 * STAGES_ <= 512) ? 2 : 1;
@@ -72,10 +76,10 @@ struct SpmmCfg {
   static constexpr int NOPS = NB * NCH * 32;  // gather4 ops per stage (one per group × chunk × block)
   static constexpr int OPS_PER_WARP = NOPS / P;
   static constexpr int LANE_OPS = (OPS_PER_WARP + 31) / 32;
-  // warp roles: [0,P) producers, P MMA, P+1..P+4 epilogue, P+5..P+8 metadata; epilogue and
+  // warp roles: [0,P) producers, P MMA, P+1..P+8 epilogue, P+9..P+12 metadata; epilogue and
   // metadata warps address TMEM lane quarter (warp % 4)
-  static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 5;
-  static constexpr int NUM_THREADS = 32 * (P + 9);
+  static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 9, EPI_WARPS = 8;
+  static constexpr int NUM_THREADS = 32 * (P + (PRE_ ? 9 : 13));
   static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
   static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
   static constexpr int BAR_BYTES = 256;
@@ -166,6 +170,13 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
       if (lane == 0 && !(p.dbg & 2)) {  // ablation 2: no MMAs (commits only)
         const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
         const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * stage;
+        if constexpr (Cfg::PRE) {
+          // pre-ordered metadata block of this stage: SMEM [128 lanes][16 B] -> 4 TMEM columns;
+          // tcgen05.cp and the MMAs below execute in issue order
+          const uint64_t edesc = smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0);
+          if constexpr (CG == 2) tc_cp_128x128b_2sm(e_tmem, edesc);
+          else tc_cp_128x128b(e_tmem, edesc);
+        }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           const uint32_t e_addr = e_tmem + kb;
@@ -205,14 +216,19 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
   }
 }
 
-// Epilogue (4 warps, one TMEM lane quarter each): TMEM -> +bias (fp32) -> RNE to fp16/bf16 ->
-// 16-byte global stores; releases the accumulator buffer to the MMA warp.
+// Epilogue (8 warps: each TMEM lane quarter twice, one half of the tile's columns per warp):
+// TMEM -> +bias (fp32) -> RNE to fp16/bf16 packed in registers; the accumulator buffer is released
+// to the MMA warp as soon as it has been read, and the 16-byte global stores overlap the next
+// tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
 template <class Cfg, bool kBF16, int CG = 1>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane) {
   using namespace ptx;
   constexpr int NB = Cfg::NB, BN = Cfg::BN;
-  const int q = warp & 3;  // TMEM lane quarter this warp may access
+  constexpr int HC = BN / (Cfg::EPI_WARPS / 4);  // columns per warp
+  constexpr int NCH = (HC + 31) / 32;   // 32-column TMEM loads per warp
+  const int q = warp & 3;               // TMEM lane quarter this warp may access
+  const int h = (warp - Cfg::W_EPI) >> 2;  // column half
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
   const int r_local = 128 * static_cast<int>(rank) + 32 * q + lane;  // row within the (pair) tile
   for (int tl = 0; tl < my_tiles; ++tl) {
@@ -228,10 +244,10 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
                                   : __half2float(__ushort_as_half(p.bias[row])))
                          : 0.0f;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
-                           ab * Cfg::ACC_COLS + b * BN;
-    const int64_t col_base = static_cast<int64_t>(n_tile) * BN;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+                           ab * Cfg::ACC_COLS + b * BN + h * HC;
+    uint32_t pk[NCH][16];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
       uint32_t v[32];
       if (p.dbg & 64) {  // ablation 64: no accumulator reads
 #pragma unroll
@@ -240,21 +256,9 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
         tmem_ld_32x32b_x32(t_row + 32 * c, v);
         tmem_ld_wait();
       }
-      const int64_t col = col_base + 32 * c;
-      if (row < p.R && !(p.dbg & 4)) {  // ablation 4: no C stores
-        uint16_t* dst = p.C + row * p.ldc + col;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (col + 8 * u < p.T) {
-            uint4 o;
-            o.x = pack2<kBF16>(__uint_as_float(v[8 * u + 0]) + bv, __uint_as_float(v[8 * u + 1]) + bv);
-            o.y = pack2<kBF16>(__uint_as_float(v[8 * u + 2]) + bv, __uint_as_float(v[8 * u + 3]) + bv);
-            o.z = pack2<kBF16>(__uint_as_float(v[8 * u + 4]) + bv, __uint_as_float(v[8 * u + 5]) + bv);
-            o.w = pack2<kBF16>(__uint_as_float(v[8 * u + 6]) + bv, __uint_as_float(v[8 * u + 7]) + bv);
-            *reinterpret_cast<uint4*>(dst + 8 * u) = o;
-          }
-        }
-      }
+      for (int j = 0; j < 16; ++j)
+        pk[c][j] = pack2<kBF16>(__uint_as_float(v[2 * j]) + bv, __uint_as_float(v[2 * j + 1]) + bv);
     }
     tc_fence_before();
     __syncwarp();
@@ -262,13 +266,25 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(acce0 + 8 * ab, 0));  // pair leader
       else mbar_arrive(acce0 + 8 * ab);
     }
+    const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
+    if (row < p.R && !(p.dbg & 4)) {  // ablation 4: no C stores
+      uint16_t* dst = p.C + row * p.ldc + col_base;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (32 * c + 8 * u < HC && col_base + 32 * c + 8 * u < p.T)
+            *reinterpret_cast<uint4*>(dst + 32 * c + 8 * u) =
+                make_uint4(pk[c][4 * u], pk[c][4 * u + 1], pk[c][4 * u + 2], pk[c][4 * u + 3]);
+    }
   }
 }
 
 template <class Cfg, bool kBF16>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
-                    const __grid_constant__ CUtensorMap tm_b, const SpmmParams p) {
+                    const __grid_constant__ CUtensorMap tm_b,
+                    const __grid_constant__ CUtensorMap tm_e, const SpmmParams p) {
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN, CG = Cfg::CG;
 
@@ -291,16 +307,17 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // leader's expect_tx + metadata warps of the pair (ablation 256: metadata warps idle)
-      mbar_init(full0 + 8 * s, (p.dbg & 256) ? 1 : 1 + 4 * CG);
+      mbar_init(full0 + 8 * s, (Cfg::PRE || (p.dbg & 256)) ? 1 : 1 + 4 * CG);
       mbar_init(empty0 + 8 * s, 1);          // (multicast) MMA commit
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf0 + 8 * b, 1);           // (multicast) MMA commit
-      mbar_init(acce0 + 8 * b, 4 * CG);      // epilogue warps of the pair
+      mbar_init(acce0 + 8 * b, 8 * CG);      // epilogue warps of the pair
     }
     fence_mbar_init();
     prefetch_tmap(&tm_values);
     prefetch_tmap(&tm_b);
+    if constexpr (Cfg::PRE) prefetch_tmap(&tm_e);
   }
   if (warp == Cfg::W_MMA) {
     if constexpr (CG == 2) tmem_alloc_2sm<512>(smem_u32(tmem_base_slot));
@@ -376,11 +393,20 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           if (warp == 0 && lane == 0) {
             VENOM_TRACE_EVENT(0, it);
             // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load
-            const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES));
+            const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES) +
+                                      (p.dbg & 2048 ? 0 : Cfg::E_BYTES));  // 2048: no metadata load
             if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
             if (!(p.dbg & 16)) {
               if constexpr (CG == 2) tma_load_2d_2sm(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
               else tma_load_2d(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+            }
+            if constexpr (Cfg::PRE) if (!(p.dbg & 2048)) {
+              // this CTA's 128-row tile, k-stage ks: row block (tile·num_ks + ks)·128 of the
+              // [tiles·num_ks·128][4] u32 pre-ordered metadata
+              const uint32_t edst = sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES;
+              const int erow = ((m_tile * CG + static_cast<int>(rank)) * p.num_ks + ks) * 128;
+              if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, erow, pol_a);
+              else tma_load_2d(edst, &tm_e, fbar, 0, erow, pol_a);
             }
           }
           if (contiguous && lane == 0 && !(p.dbg & 1)) {
@@ -423,9 +449,9 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     }
   } else if (warp == Cfg::W_MMA) {
     if (rank == 0) mma_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
-  } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 4) {
+  } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 8) {
     epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane);
-  } else {
+  } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
     // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3. The warp

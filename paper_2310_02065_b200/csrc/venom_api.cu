@@ -58,6 +58,14 @@ venom_status_t validate_format(int64_t R, int64_t K, venom_format_t f) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+constexpr int kCompressThreads = 512;
+
+// ablation / debug flags for tools (VENOM_DEBUG_FLAGS; 0 in production)
+int debug_flags() {
+  const char* d = getenv("VENOM_DEBUG_FLAGS");
+  return d ? atoi(d) : 0;
+}
+
 venom_status_t launch_status() {
   return cudaGetLastError() == cudaSuccess ? VENOM_OK : VENOM_ERR_CUDA;
 }
@@ -90,8 +98,8 @@ venom_status_t launch_cg(Kern kern, int cg, int grid, int threads, int smem, cud
 
 // ------------------------------------------------------------------ SpMM dispatch
 template <class Cfg, bool kBF16>
-venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams p, int max_ctas,
-                        cudaStream_t s) {
+venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUtensorMap& te,
+                        SpmmParams p, int max_ctas, cudaStream_t s) {
   auto kern = venom::vnm_spmm_kernel<Cfg, kBF16>;
   // >= 116 KB of shared memory guarantees one CTA per SM (each CTA allocates all 512 TMEM columns)
   const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
@@ -105,14 +113,37 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams
   int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid < 1) return VENOM_OK;
-  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, p);
+  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, te, p);
 }
 
 template <class Cfg>
-venom_status_t run_spmm_dt(bool bf16, const CUtensorMap& tv, const CUtensorMap& tb, SpmmParams p,
-                           int max_ctas, cudaStream_t s) {
-  return bf16 ? run_spmm<Cfg, true>(tv, tb, p, max_ctas, s)
-              : run_spmm<Cfg, false>(tv, tb, p, max_ctas, s);
+venom_status_t run_spmm_dt(bool bf16, const CUtensorMap& tv, const CUtensorMap& tb,
+                           const CUtensorMap& te, SpmmParams p, int max_ctas, cudaStream_t s) {
+  return bf16 ? run_spmm<Cfg, true>(tv, tb, te, p, max_ctas, s)
+              : run_spmm<Cfg, false>(tv, tb, te, p, max_ctas, s);
+}
+
+// Gathered / contiguous kernel configurations. PRE: metadata pre-ordered for the tensor core.
+template <bool PRE>
+venom_status_t run_gather(int NBg, int pair, int tile_t, bool bf16, const CUtensorMap& tv,
+                          const CUtensorMap& tb, const CUtensorMap& te, SpmmParams p, int max_ctas,
+                          cudaStream_t s) {
+  using namespace venom;
+  if (NBg == 1 && pair == 2) {
+    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 4, 8, 2, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 6, 8, 2, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+  } else if (NBg == 1) {
+    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+    if (tile_t == 192) return run_spmm_dt<SpmmCfg<1, 192, 3, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<1, 64, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+  } else if (NBg == 2) {
+    if (tile_t == 128) return run_spmm_dt<SpmmCfg<2, 128, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<2, 64, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+  } else {
+    if (tile_t == 64) return run_spmm_dt<SpmmCfg<4, 64, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
+  }
+  return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
 }
 
 template <class Cfg, bool kBF16>
@@ -229,11 +260,43 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
   if (!aligned(values, 8) || !aligned(column_idx, 4) || !aligned(A, 2)) return VENOM_ERR_INVALID_ARGUMENT;
   if ((st = check_arch()) != VENOM_OK) return st;
   const int64_t G = K / f.m;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  {
+    // shared-memory tile kernel: ~256 columns per CTA (even number of groups, W % 8 == 0), the
+    // V × W tile at most 64 KB; narrower chunks when the grid would have < 2 CTAs per SM
+    int gt = 256 / f.m;
+    gt -= gt & 1;
+    if (gt < 2) gt = 2;
+    while ((gt * f.m) % 8 != 0) gt += 2;
+    while (gt > 2 && static_cast<int64_t>(f.v) * gt * f.m * 2 > 65536) gt -= 2;
+    while ((gt * f.m) % 8 != 0 && gt > 2) gt -= 2;
+    if (gt > G + (G & 1)) gt = static_cast<int>(G + (G & 1));
+    while ((gt * f.m) % 8 != 0) gt += 2;  // pitch alignment (may exceed G: extra columns unused)
+    while (gt >= 8 && ((G + gt - 1) / gt) * (R / f.v) < 2 * 148 && ((gt / 2) * f.m) % 8 == 0 &&
+           (gt / 2) % 2 == 0)
+      gt /= 2;
+    const size_t tsmem = ((static_cast<size_t>(f.v) * gt * f.m * 2 + 15) & ~size_t(15)) +
+                         8 * static_cast<size_t>(gt) * f.m + 4 * static_cast<size_t>(gt);
+    if (tsmem <= 100 * 1024 && (R / f.v) <= 65535) {
+      const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
+      auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, false>
+                                     : venom::vnm_compress_tile_kernel<false, false>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)) != cudaSuccess)
+        return VENOM_ERR_CUDA;
+      kern<<<grid, kCompressThreads, tsmem, s>>>(static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gt,
+                                    static_cast<uint16_t*>(values), metadata, column_idx, dev_status,
+                                    nullptr, nullptr, debug_flags());
+      return launch_status();
+    }
+  }
+  // very tall blocks: streaming kernel (partial sums over row ranges, no tile copy)
   // ~256 columns per CTA (whole, even number of groups), so that R/V × K/256 CTAs stream A
   int gpc = 256 / f.m;
   gpc -= gpc & 1;
   if (gpc < 2) gpc = 2;
   if (gpc > G + (G & 1)) gpc = static_cast<int>(G + (G & 1));
+  // latency hiding: at least ~4 CTAs per SM (narrower column chunks when R/V × K/256 is small)
+  while (gpc >= 4 && ((G + gpc - 1) / gpc) * (R / f.v) < 4 * 148) gpc = (gpc / 2) & ~1;
   const bool vec = aligned(A, 16) && (lda % 8 == 0) && ((static_cast<int64_t>(gpc) * f.m) % 8 == 0);
   const dim3 grid(static_cast<unsigned>((G + gpc - 1) / gpc), static_cast<unsigned>(R / f.v));
   if (grid.y > 65535u) return VENOM_ERR_INVALID_ARGUMENT;
@@ -242,7 +305,6 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
   const int ncv_max = (wmax + vecw - 1) / vecw;
   const int nsplit_max = (dt == VENOM_BF16) ? 1 : (256 / ncv_max > 0 ? 256 / ncv_max : 1);
   const size_t smem = sizeof(double) * static_cast<size_t>(nsplit_max) * wmax + 4 * static_cast<size_t>(gpc);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
 #define VENOM_COMPRESS(BF, VW)                                                                     \
   venom::vnm_compress_kernel<BF, VW><<<grid, 256, smem, s>>>(                                      \
       static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values), \
@@ -253,6 +315,43 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
     if (vec) VENOM_COMPRESS(false, 8); else VENOM_COMPRESS(false, 1);
   }
 #undef VENOM_COMPRESS
+  return launch_status();
+}
+
+venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t lda, venom_dtype_t dt,
+                                  venom_format_t f, void* values, uint8_t* metadata,
+                                  uint8_t* column_idx, void* values_2to4, uint8_t* metadata_2to4_tc,
+                                  int32_t* dev_status, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (f.m % 8 != 0 || 128 % f.m != 0 || f.v % 16 != 0 || K % 16 != 0 || f.v > 256)
+    return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (lda < K) return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!A || !values || !metadata || !column_idx || !values_2to4 || !metadata_2to4_tc)
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(values, 8) || !aligned(column_idx, 4) || !aligned(A, 2) || !aligned(values_2to4, 16) ||
+      !aligned(metadata_2to4_tc, 16))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (R / f.v > 65535) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  // whole k-stages of the re-encoded operand per CTA: W = gt·M a multiple of 128 columns
+  const int W = (f.v <= 128 && !(debug_flags() & 16)) ? 256 : 128;
+  const int gt = W / f.m > 0 ? W / f.m : 1;
+  if (gt * f.m != W) return VENOM_ERR_UNSUPPORTED_PATTERN;  // M must divide W (M | 128)
+  const size_t tsmem = ((static_cast<size_t>(f.v) * W * 2 + 15) & ~size_t(15)) + 8 * static_cast<size_t>(W) +
+                       4 * static_cast<size_t>(gt) + static_cast<size_t>(f.v) * (W / 8);
+  const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
+  auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, true>
+                                 : venom::vnm_compress_tile_kernel<false, true>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)) != cudaSuccess)
+    return VENOM_ERR_CUDA;
+  kern<<<grid, (debug_flags() & 32) ? 256 : kCompressThreads, tsmem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gt, static_cast<uint16_t*>(values),
+      metadata, column_idx, dev_status, static_cast<uint32_t*>(values_2to4),
+      reinterpret_cast<uint32_t*>(metadata_2to4_tc), debug_flags());
   return launch_status();
 }
 
@@ -274,8 +373,23 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
   const int kv = vec ? 8 : 1;
   const int64_t chunks = (K + kv - 1) / kv;
   if (K > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
-  const dim3 grid(static_cast<unsigned>((chunks + 255) / 256),
-                  static_cast<unsigned>(R < 65535 ? R : 65535));
+  if (R * chunks >= 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  const int64_t blocks = (R * chunks + 255) / 256;
+  const dim3 grid(static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64));
+  if (vec && f.m % 8 == 0 && R <= 0x7FFFFFFF) {
+    const dim3 g2(static_cast<unsigned>((K / 8 + 255) / 256), static_cast<unsigned>(R < 65535 ? R : 65535));
+#define VENOM_DEC8(C)                                                                                  \
+  venom::vnm_decompress_m8_kernel<C><<<g2, 256, 0, s>>>(                                               \
+      static_cast<const uint32_t*>(values), metadata, reinterpret_cast<const uint32_t*>(column_idx), \
+      static_cast<int>(R), static_cast<int>(K), f.v, f.m, static_cast<int>(G),                        \
+      static_cast<uint16_t*>(A_out), lda, dev_status)
+    if (f.m == 8) VENOM_DEC8(1);
+    else if (f.m == 16) VENOM_DEC8(2);
+    else if (f.m == 32) VENOM_DEC8(4);
+    else VENOM_DEC8(0);
+#undef VENOM_DEC8
+    return launch_status();
+  }
   if (vec)
     venom::vnm_decompress_kernel<8><<<grid, 256, 0, s>>>(
         static_cast<const uint16_t*>(values), metadata, column_idx, R, K, f.v, f.m, G,
@@ -290,6 +404,8 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
 int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f) {
   if (validate_format(R, K, f) != VENOM_OK || f.m % 4 != 0 || f.m == 4) return 0;
   if ((K / 4) % 4 != 0 || T < 256) return 0;
+  // the fused preparation (venom_compress_2to4) must apply
+  if (f.m % 8 != 0 || 128 % f.m != 0 || f.v % 16 != 0 || f.v > 256 || K % 16 != 0) return 0;
   // measured crossover: the gathered path is bound by the gather feed,
   // whose bytes per useful FLOP grow as 1/V, while the 2:4 CTA-pair path streams dense B tiles
   // at twice the useful work; below V·M ≈ 1536 the 2:4 form wins
@@ -314,7 +430,9 @@ venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,
   if ((st = check_arch()) != VENOM_OK) return st;
   const int64_t G = K / f.m;
   const int64_t npairs = (G + 1) / 2;
-  const dim3 grid(static_cast<unsigned>((npairs + 255) / 256), static_cast<unsigned>(R < 65535 ? R : 65535));
+  if (R * npairs >= 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
+  const int64_t blocks = (R * npairs + 255) / 256;
+  const dim3 grid(static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64));
   venom::vnm_expand_2to4_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint32_t*>(values), metadata, reinterpret_cast<const uint32_t*>(column_idx), R,
       f.v, f.m, G, static_cast<uint32_t*>(values_out), metadata_out,
@@ -341,7 +459,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (T < 0 || ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
     return VENOM_ERR_INVALID_ARGUMENT;
   if (R == 0 || T == 0) return VENOM_OK;
-  if (!C || (K > 0 && (!values || !metadata || !column_idx || !B))) return VENOM_ERR_INVALID_ARGUMENT;
+  const bool has_tc = opts && opts->metadata_tc;
+  // metadata is not read with pre-ordered metadata; column_idx is not read when M = 4 (identity)
+  if (!C || (K > 0 && (!values || !B || (!metadata && !has_tc) || (!column_idx && f.m != 4))))
+    return VENOM_ERR_INVALID_ARGUMENT;
   if (!aligned(C, 16) || (K > 0 && (!aligned(values, 16) || !aligned(B, 16) || !aligned(column_idx, 4))))
     return VENOM_ERR_INVALID_ARGUMENT;
   if (K > 0x7FFFFFFF || T > 0x7FFFFFFF || R > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
@@ -409,6 +530,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
 
+  if (use_densek && (!metadata || !column_idx)) return VENOM_ERR_INVALID_ARGUMENT;
   if (use_densek) {
     // B: 2-D [K rows][T], box 64 columns × 128 rows (one K-stage of one 64-column chunk), SW128
     CUtensorMap tb;
@@ -451,22 +573,49 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (pair == 2 && !pair_ok) return VENOM_ERR_INVALID_ARGUMENT;
   if (tile_t == 0) tile_t = (NBg == 1) ? 256 : (NBg == 2 ? 128 : 64);
   set_tiles(tile_t);
-  if (NBg == 1 && pair == 2) {
-    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 4, 8, 2>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 6, 8, 2>>(bf16, tv, tb, p, max_ctas, s);
-  } else if (NBg == 1) {
-    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 192) return run_spmm_dt<SpmmCfg<1, 192, 3>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 4>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<1, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
-  } else if (NBg == 2) {
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<2, 128, 2>>(bf16, tv, tb, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<2, 64, 4>>(bf16, tv, tb, p, max_ctas, s);
-  } else {
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<4, 64, 2>>(bf16, tv, tb, p, max_ctas, s);
-  }
   (void)stages;
-  return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
+  const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
+  if (meta_tc == nullptr) return run_gather<false>(NBg, pair, tile_t, bf16, tv, tb, tv, p, max_ctas, s);
+  // pre-ordered metadata: 2-D [tiles·num_ks·128 rows][4] u32, box 4 × 128 (one 2 KB stage block)
+  if (!aligned(meta_tc, 16)) return VENOM_ERR_INVALID_ARGUMENT;
+  CUtensorMap te;
+  {
+    const int64_t rows = ((R + 127) / 128) * p.num_ks * 128;
+    cuuint64_t dims[2] = {4, static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {16};
+    cuuint32_t box[2] = {4, 128};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(meta_tc), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  }
+  return run_gather<true>(NBg, pair, tile_t, bf16, tv, tb, te, p, max_ctas, s);
+}
+
+int64_t venom_metadata_tc_bytes(int64_t R, int64_t K, venom_format_t f) {
+  if (validate_format(R, K, f) != VENOM_OK) return -1;
+  const int64_t G = K / f.m;
+  return ((R + 127) / 128) * ((G + 31) / 32) * 128 * 16;
+}
+
+venom_status_t venom_order_metadata(const uint8_t* metadata, int64_t R, int64_t K, venom_format_t f,
+                                    uint8_t* metadata_tc, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  if (G % 4 != 0) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!metadata || !metadata_tc || !aligned(metadata_tc, 16) || !aligned(metadata, 2))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t num_ks = (G + 31) / 32;
+  const int64_t total = ((R + 127) / 128) * num_ks * 128 * 4;  // 32-bit words
+  const int64_t blocks = (total + 255) / 256;
+  venom::vnm_order_metadata_kernel<<<static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0,
+                                     static_cast<cudaStream_t>(stream)>>>(
+      metadata, R, G, num_ks, total, reinterpret_cast<uint32_t*>(metadata_tc));
+  return launch_status();
 }
 
 venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

@@ -73,6 +73,33 @@ def test_expand_argument_errors(L):
     assert ex(n=1) == 4
 
 
+def test_metadata_tc_sizes_and_errors(L):
+    P = ctypes.c_void_p
+    f = venom._Format
+    assert L.venom_metadata_tc_bytes(1024, 4096, f(64, 2, 8)) == 8 * 16 * 128 * 16  # 8 tiles, 16 k-stages
+    assert L.venom_metadata_tc_bytes(130, 320, f(13, 2, 10)) == 2 * 1 * 128 * 16
+    assert L.venom_metadata_tc_bytes(130, 320, f(7, 2, 10)) == -1  # V does not divide R
+    fake = P(0x10000)
+    assert L.venom_order_metadata(fake, 256, 8 * 6, f(64, 2, 8), fake, P(0)) == 4  # G % 4 != 0
+    assert L.venom_order_metadata(fake, 256, 500, f(64, 2, 8), fake, P(0)) == 3
+    assert L.venom_order_metadata(fake, 256, 512, f(64, 2, 8), P(0x10008), P(0)) == 1  # misaligned
+
+
+def test_compress_2to4_argument_errors(L):
+    P = ctypes.c_void_p
+    fake = P(0x10000)
+
+    def c24(R=256, K=512, V=64, M=8, lda=512, dt=0):
+        return L.venom_compress_2to4(fake, R, K, lda, dt, venom._Format(V, 2, M), fake, fake, fake, fake,
+                                     fake, P(0), P(0))
+    assert c24(M=4) == 4          # nothing to re-encode (M % 8)
+    assert c24(V=24, R=240) == 4  # V % 16
+    assert c24(M=24, K=24 * 20, lda=480) == 4  # M does not divide 128
+    assert c24(R=200) == 2
+    assert c24(lda=100) == 1
+    assert c24(dt=3) == 5
+
+
 def test_spmm_argument_errors(L):
     assert _spmm(L, R=384, V=96, K=640, M=10) == 4   # gather: V not in {32,64} ∪ 128N; dense-K: M ∤ 128
     assert _spmm(L, K=12 * 6, M=12) == 4       # gather: G = 6 not a multiple of 4; dense-K: M = 12

@@ -207,9 +207,13 @@ def test_spmm_identity_probe_exact():
         vals, meta, cidx = oracle.compress(A, dt, V=V, M=M)
         D = oracle.decompress(vals, meta, cidx, R, K, dt, V, M)
         I = to_dev(f64_to_bits(np.eye(K), dt), dt)
-        C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), I)
-        got = bits_to_f64(to_bits(C), dt)
-        assert np.array_equal(got, bits_to_f64(D, dt)), (R, K, V, M, dt)
+        x = vnm_from((vals, meta, cidx), R, K, V, M, dt)
+        for prepared in (False, True):
+            if prepared:
+                venom.order_metadata(x)
+            C = venom.spmm(x, I)
+            got = bits_to_f64(to_bits(C), dt)
+            assert np.array_equal(got, bits_to_f64(D, dt)), (R, K, V, M, dt, prepared)
 
 
 def test_spmm_one_hot_probes():
@@ -223,9 +227,13 @@ def test_spmm_one_hot_probes():
     ks = np.random.Generator(np.random.PCG64(5)).choice(K, size=T, replace=False)
     Bm = np.zeros((K, T))
     Bm[ks, np.arange(T)] = 1.0
-    C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), to_dev(f64_to_bits(Bm, dt), dt))
-    got = bits_to_f64(to_bits(C), dt)
-    assert np.array_equal(got, D[:, ks])
+    x = vnm_from((vals, meta, cidx), R, K, V, M, dt)
+    for prepared in (False, True):
+        if prepared:
+            venom.order_metadata(x)
+        C = venom.spmm(x, to_dev(f64_to_bits(Bm, dt), dt))
+        got = bits_to_f64(to_bits(C), dt)
+        assert np.array_equal(got, D[:, ks]), prepared
 
 
 SPMM_CASES = [
@@ -266,6 +274,13 @@ def test_spmm_vs_oracle(R, K, T, V, M, dt, bias, tile_t):
         C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tt,
                        strategy=strat)
         check_spmm(C, C_ref, dt)
+    # tensor-core-ordered metadata (TMA + tcgen05.cp path), every CTA grouping that applies
+    venom.order_metadata(x)
+    pairs = [0, 1] + ([2] if M == 4 or V % 256 == 0 else [])
+    for pair in pairs:
+        C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tile_t,
+                       strategy=venom.STRATEGY_GATHER, cta_pair=pair)
+        check_spmm(C, C_ref, dt)
 
 
 DENSEK_CASES = [
@@ -300,6 +315,66 @@ def test_spmm_identity_probe_exact_densek():
         I = to_dev(f64_to_bits(np.eye(K), dt), dt)
         C = venom.spmm(vnm_from((vals, meta, cidx), R, K, V, M, dt), I, strategy=venom.STRATEGY_DENSE_K)
         assert np.array_equal(bits_to_f64(to_bits(C), dt), bits_to_f64(D, dt)), (R, K, V, M, dt)
+
+
+def tc_order(meta: np.ndarray, R: int, G: int) -> np.ndarray:
+    """The tensor-core metadata order include/venom.h states, written out: uint32[mt][ks][L][kb]."""
+    nks = (G + 31) // 32
+    mt_n = (R + 127) // 128
+
+    def half(row, g0):
+        if row >= R or g0 >= G:
+            return 0x4444
+        return int(meta[row, g0 // 2]) | (int(meta[row, g0 // 2 + 1]) << 8)
+    exp = np.zeros((mt_n, nks, 128, 4), np.uint32)
+    for mt in range(mt_n):
+        for ks in range(nks):
+            for L in range(128):
+                ra = mt * 128 + (L & 7) + 16 * (L >> 4)
+                for kb in range(4):
+                    g0 = ks * 32 + kb * 8 + 4 * ((L >> 3) & 1)
+                    exp[mt, ks, L, kb] = half(ra, g0) | (half(ra + 8, g0) << 16)
+    return exp
+
+
+@pytest.mark.parametrize("R,K,V,M", [(256, 512, 128, 8), (200, 256, 8, 4), (64, 1280, 64, 40),
+                                     (384, 640, 128, 20)])
+def test_order_metadata_layout(R, K, V, M):
+    """venom_order_metadata against the permutation include/venom.h states."""
+    A = synth.gaussian((R, K), 1.0, F16, 31)
+    vals, meta, cidx = oracle.compress(A, F16, V=V, M=M)
+    x = vnm_from((vals, meta, cidx), R, K, V, M, F16)
+    venom.order_metadata(x)
+    exp = tc_order(meta, R, K // M)
+    assert np.array_equal(x.metadata_tc.cpu().numpy().view(np.uint32).reshape(exp.shape), exp)
+
+
+@pytest.mark.parametrize("R,K,V,M,kind,dt", [
+    (1024, 4096, 64, 8, "gauss", F16),      # BERT-large FFN2 shape
+    (192, 1040, 64, 8, "int", F16),         # ragged last row tile; partial last k-stage
+    (256, 768, 256, 16, "gauss", BF16),     # V = 256 (128-column CTA chunks)
+    (96, 512, 32, 32, "special", F16),      # V = 32, ragged rows
+    (160, 384, 16, 8, "sparse", BF16),      # V = 16
+])
+def test_compress_2to4_fused(R, K, V, M, kind, dt):
+    """venom_compress_2to4 == venom_compress (bit-exact canonical arrays) + the oracle's V:2:4
+    re-encoding (values) + the tensor-core order of the re-encoded metadata; SpMM on it == oracle."""
+    A = make_input(R, K, kind, dt, 13 + R + K, M)
+    parts = oracle.compress(A, dt, V=V, M=M)
+    v2, m2, c2 = oracle.expand_2to4(*parts, R, K, V, M)
+    x, y = venom.compress_2to4(to_dev(A, dt), V=V, M=M, check=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_bits(x.values).reshape(parts[0].shape), parts[0])
+    assert np.array_equal(x.metadata.cpu().numpy(), parts[1])
+    assert np.array_equal(x.column_idx.cpu().numpy(), parts[2])
+    assert np.array_equal(to_bits(y.values).reshape(v2.shape), v2)
+    exp = tc_order(m2, R, K // 4)
+    assert np.array_equal(y.metadata_tc.cpu().numpy().view(np.uint32)[:exp.size].reshape(exp.shape), exp)
+    if kind != "special":  # max-finite inputs overflow the fp16 product legitimately
+        T = 136
+        B = synth.gaussian((K, T), 1.0, dt, 14 + R)
+        C = venom.spmm(y, to_dev(B, dt))
+        check_spmm(C, oracle.spmm(*parts, R, K, dt, V, M, B), dt)
 
 
 def test_spmm_ldb_ldc_views_and_shard_equality():
@@ -383,3 +458,10 @@ def test_spmm_full_size_bert_sampled(wl):
     for strat in strategies(K, V, M):
         C = venom.spmm(x, Bd, strategy=strat)
         check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)
+    # bench.py's launch configuration: planner-chosen operand form + tensor-core-ordered metadata
+    if venom.prefers_2to4(R, K, T, V, M):
+        x2, y = venom.compress_2to4(to_dev(A, F16), V=V, M=M, check=True)
+    else:
+        y = venom.order_metadata(x)
+    C = venom.spmm(y, Bd)
+    check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)

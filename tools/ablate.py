@@ -8,10 +8,13 @@ import paper_2310_02065_b200 as venom
 
 R, K, T, V, M, strat, pair = (int(x) for x in sys.argv[1:8])
 flags = [int(x) for x in sys.argv[8:]] or [0]
+prepared = os.environ.get("PREPARED", "1") == "1"
 torch.manual_seed(0)
 A = (torch.randn(R, K, device="cuda") * 0.02).half()
 B = torch.randn(K, T, device="cuda").half()
 x = venom.compress(A, V=V, M=M, check=True)
+if prepared:
+    venom.order_metadata(x)
 C = torch.empty(R, T, device="cuda", dtype=torch.half)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for fl in flags:
