@@ -83,7 +83,8 @@ struct SpmmCfg {
   static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
   static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
+  static constexpr int EPI_STAGE_BYTES = 2048;  // per epilogue warp: 32 rows × 64 B output chunk
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_WARPS * EPI_STAGE_BYTES;
   static_assert(BNH % 64 == 0 && BN <= 256, "BN");
   static_assert(E_COL + 4 * STAGES_ <= 512, "TMEM budget");
   static_assert(STAGE_BYTES % 1024 == 0, "stage alignment");
@@ -222,7 +223,8 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 // tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
 template <class Cfg, bool kBF16, int CG = 1>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
-                                              uint32_t accf0, uint32_t acce0, int warp, int lane) {
+                                              uint32_t accf0, uint32_t acce0, int warp, int lane,
+                                              uint32_t stage_smem = 0) {
   using namespace ptx;
   constexpr int NB = Cfg::NB, BN = Cfg::BN;
   constexpr int HC = BN / (Cfg::EPI_WARPS / 4);  // columns per warp
@@ -267,7 +269,35 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       else mbar_arrive(acce0 + 8 * ab);
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
-    if (row < p.R && !(p.dbg & 4)) {  // ablation 4: no C stores
+    if (p.dbg & 4) {  // ablation 4: no C stores
+    } else if (stage_smem != 0) {
+      // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
+      // store instruction writes 8 rows × 64 contiguous bytes (full sectors) instead of 32 rows ×
+      // 16 bytes; 16-byte segments XOR-swizzled by row to keep both passes bank-conflict free
+      const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG) + 128 * static_cast<int>(rank) + 32 * q;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (32 * c >= HC) break;
+#pragma unroll
+        for (int sgm = 0; sgm < 4; ++sgm) {
+          const uint32_t a = stage_smem + lane * 64 + ((sgm ^ ((lane >> 1) & 3)) * 16);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c][4 * sgm]),
+                       "r"(pk[c][4 * sgm + 1]), "r"(pk[c][4 * sgm + 2]), "r"(pk[c][4 * sgm + 3]) : "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 8 * j + (lane >> 2), sgm = lane & 3;
+          uint4 o;
+          const uint32_t a = stage_smem + r * 64 + ((sgm ^ ((r >> 1) & 3)) * 16);
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
+          const int64_t orow = row_base + r;
+          const int64_t ocol = col_base + 32 * c + 8 * sgm;
+          if (orow < p.R && ocol < p.T) *reinterpret_cast<uint4*>(p.C + orow * p.ldc + ocol) = o;
+        }
+        __syncwarp();
+      }
+    } else if (row < p.R) {
       uint16_t* dst = p.C + row * p.ldc + col_base;
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
@@ -450,7 +480,9 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   } else if (warp == Cfg::W_MMA) {
     if (rank == 0) mma_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 8) {
-    epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane);
+    epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane,
+                                  smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES +
+                                      (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
