@@ -50,6 +50,11 @@ for _k in synth.WORKLOADS:
 DEFAULT_WORKLOAD = "bert_large_ffn_4096tok_64:2:8"
 
 
+# measured TMA L2 -> SMEM landing ceiling per SM (GB/s): tools/microbench_stream.cu,
+# profiles/r01_microbench_stream.txt (64.8-65.2 B/ns per SM with multicast, 49 without)
+FEED_CEILING_GBPS_PER_SM = 65.0
+
+
 def useful_flops(w) -> float:
     """2·nnz·T with nnz = R·K·2/M (values are R×K/M×2)."""
     return 2.0 * (w["R"] * (w["K"] // w["M"]) * 2) * w["T"]
@@ -269,20 +274,31 @@ def run_gpu(args, ws, rank, local):
     spmm_flops = [L.flops for L in layers]
     achieved = sum(spmm_flops) / (sum(per_launch_ms) / 1e3) / 1e12
     peak_burst, peak_sust, hbm, peak_src = load_peaks()
-    traffic = None
+    traffic, feed = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f).get(args.workload)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
+            xb = tr.get("l2_to_smem_bytes_per_launch")
+            if xb and len(xb) == len(per_launch_ms):
+                # the on-chip feed that binds these kernels: L2 -> SMEM bytes per
+                # launch (ncu l1tex__m_xbar2l1tex_read_bytes) over the live launch time, against the
+                # measured per-SM landing ceiling × SMs (tools/microbench_stream.cu)
+                ach = sum(xb) / (sum(per_launch_ms) / 1e3) / 1e9
+                ceil = FEED_CEILING_GBPS_PER_SM * torch.cuda.get_device_properties(device).multi_processor_count
+                feed = {"l2_to_smem_bytes_per_launch": xb, "achieved_GBps": round(ach, 1),
+                        "ceiling_GBps": round(ceil, 1), "frac": round(ach / ceil, 4),
+                        "ceiling_source": "profiles/r01_microbench_stream.txt (TMA landing, multicast)"}
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_burst, 4), "traffic": traffic,
                 "peak_source": f"{peak_src} bf16 dense burst (fp16 1:1); useful FLOPs of a 2:4 sparse "
                                f"MMA are half its issued FLOPs, so the useful-FLOP peak equals the dense peak",
                 "algorithmic_flops_per_launch": [int(x) for x in spmm_flops],
                 "mean_launch_ms": [round(x, 5) for x in per_launch_ms],
-                "hbm_frac": round(sum(algorithmic_bytes(L.w) for L in layers) / (sum(per_launch_ms) / 1e3) / 1e9 / hbm, 4)}
+                "hbm_frac": round(sum(algorithmic_bytes(L.w) for L in layers) / (sum(per_launch_ms) / 1e3) / 1e9 / hbm, 4),
+                "feed": feed}
 
     # cuBLAS dense fp16 baseline at the same shapes (speedup metric)
     torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False

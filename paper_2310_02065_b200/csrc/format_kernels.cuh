@@ -242,14 +242,31 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
   const int nvec = ncols / 8;  // full 8-column vectors of a row (W % 8 == 0 by construction)
   const bool vec_ok = ((lda & 7) == 0) && ((k0 & 7) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   if (vec_ok && !(dbg & 1)) {
-    for (int t = threadIdx.x; t < V * nvec; t += blockDim.x) {
-      const int i = t / nvec, cv = t - i * nvec;
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(A + (row0 + i) * lda + k0) + cv);
-      *reinterpret_cast<uint4*>(tile + i * W + 8 * cv) = w;
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+    // 4 independent 16-byte loads in flight per thread before any of them is consumed
+    constexpr int U = 4;
+    const int nv = V * nvec;
+    for (int t0 = threadIdx.x; t0 < nv; t0 += U * blockDim.x) {
+      uint4 w[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        bad |= bits_non_finite<kBF16>(static_cast<uint16_t>((ww[u >> 1] >> (16 * (u & 1))) & 0xFFFFu));
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * static_cast<int>(blockDim.x);
+        if (t < nv) {
+          const int i = t / nvec, cv = t - i * nvec;
+          w[u] = __ldg(reinterpret_cast<const uint4*>(A + (row0 + i) * lda + k0) + cv);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * static_cast<int>(blockDim.x);
+        if (t < nv) {
+          const int i = t / nvec, cv = t - i * nvec;
+          *reinterpret_cast<uint4*>(tile + i * W + 8 * cv) = w[u];
+          const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            bad |= bits_non_finite<kBF16>(static_cast<uint16_t>((ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu));
+        }
+      }
     }
   }
   const int cstart = vec_ok ? 8 * nvec : 0;

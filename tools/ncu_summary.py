@@ -33,14 +33,16 @@ def full(rep, out, key=None):
         try:
             rb = float(d["dram__bytes_read.sum"]); wb = float(d["dram__bytes_write.sum"])
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            traffic.append(rb * scale.get(u["dram__bytes_read.sum"], 1) + wb * scale.get(u["dram__bytes_write.sum"], 1))
+            xb = float(d["l1tex__m_xbar2l1tex_read_bytes.sum"]) * scale.get(u["l1tex__m_xbar2l1tex_read_bytes.sum"], 1)
+            traffic.append((rb * scale.get(u["dram__bytes_read.sum"], 1) + wb * scale.get(u["dram__bytes_write.sum"], 1), xb))
         except Exception:
             pass
     open(out, "w").write("\n".join(lines) + "\n")
     if key and traffic:
         p = os.path.join(os.path.dirname(out), "ncu_traffic.json")
         j = json.load(open(p)) if os.path.exists(p) else {}
-        j[key] = {"dram_bytes_per_launch": sum(traffic) / len(traffic), "launches": len(traffic),
+        j[key] = {"dram_bytes_per_launch": sum(t[0] for t in traffic) / len(traffic),
+                  "l2_to_smem_bytes_per_launch": [t[1] for t in traffic], "launches": len(traffic),
                   "source": os.path.basename(rep)}
         json.dump(j, open(p, "w"), indent=1)
     print("\n".join(lines))
