@@ -217,13 +217,27 @@ def run_gpu(args, ws, rank, local):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
 
+    side = torch.cuda.Stream(device)  # decompress (a4) overlaps the SpMMs on a second stream
+
     def step(spmm_events=None, part_events=None):
+        stream = torch.cuda.current_stream(device)  # the capture stream when recording a graph
         if part_events is not None:
             part_events[0].record(stream)
         for L in layers:
             L.compress()
         if part_events is not None:
             part_events[1].record(stream)
+        if args.step == "full" and args.overlap:
+            # a4 depends only on this layer's compression: run it beside the SpMMs (idle SMs of
+            # the persistent SpMM grid take it), joined before the step ends
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                if part_events is not None:
+                    part_events[2].record(side)
+                for i, L in enumerate(layers):
+                    L.decompress()
+                if part_events is not None:
+                    part_events[3].record(side)
         for i, L in enumerate(layers):
             if spmm_events is not None:
                 spmm_events[i][0].record(stream)
@@ -231,12 +245,15 @@ def run_gpu(args, ws, rank, local):
             if spmm_events is not None:
                 spmm_events[i][1].record(stream)
         if args.step == "full":
-            if part_events is not None:
-                part_events[2].record(stream)
-            for L in layers:
-                L.decompress()
-            if part_events is not None:
-                part_events[3].record(stream)
+            if args.overlap:
+                stream.wait_stream(side)
+            else:
+                if part_events is not None:
+                    part_events[2].record(stream)
+                for L in layers:
+                    L.decompress()
+                if part_events is not None:
+                    part_events[3].record(stream)
 
     # [compress_2to4 | compress + order_metadata] + spmm (+ decompress) per layer
     launches_per_step = sum((1 if L.expand else 2) + 1 + int(args.step == "full") for L in layers)
@@ -244,6 +261,17 @@ def run_gpu(args, ws, rank, local):
         flush.zero_()
         step()
     torch.cuda.synchronize(device)
+    graph = None
+    if args.graph:
+        # the whole step as one CUDA graph (both streams): no per-launch CPU/driver gaps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize(device)
+        for _ in range(2):
+            flush.zero_()
+            graph.replay()
+        torch.cuda.synchronize(device)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sp_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in layers]
@@ -252,15 +280,29 @@ def run_gpu(args, ws, rank, local):
     clocks = ClockSampler(device.index if device.index is not None else 0)
     barrier(ws)
     torch.cuda.synchronize(device)
+    # eager pass: per-kernel events (roofline per launch, step breakdown)
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record(stream)
         step(sp_ev[k], pt_ev[k])
         ev[k][1].record(stream)
     torch.cuda.synchronize(device)
+    eager_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = eager_ms
+    if graph is not None:
+        # timed pass: the captured step replayed K times (L2 flushed before each)
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier(ws)
+        torch.cuda.synchronize(device)
+        for k in range(args.steps):
+            flush.zero_()
+            gev[k][0].record(stream)
+            graph.replay()
+            gev[k][1].record(stream)
+        torch.cuda.synchronize(device)
+        step_ms = [a.elapsed_time(b) for a, b in gev]
     barrier(ws)
     clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     spmm_ms = [[a.elapsed_time(b) for a, b in row] for row in sp_ev]
     compress_ms = statistics.mean(r[0].elapsed_time(r[1]) for r in pt_ev)
     decompress_ms = statistics.mean(r[2].elapsed_time(r[3]) for r in pt_ev) if args.step == "full" else 0.0
@@ -378,6 +420,9 @@ def run_gpu(args, ws, rank, local):
             "step_breakdown_ms": {"compress_all_layers": round(compress_ms, 5),
                                   "spmm_all_layers": round(sum(per_launch_ms), 5),
                                   "decompress_all_layers": round(decompress_ms, 5),
+                                  "decompress_overlapped": bool(args.overlap and args.step == "full"),
+                                  "eager_step_ms": round(statistics.mean(eager_ms), 5),
+                                  "timed_as": "CUDA graph replay of the step" if graph is not None else "eager step",
                                   "compress_GBps": round(sum(2 * L.w["R"] * L.w["K"] for L in layers) / compress_ms / 1e6, 1)},
             "speedup_vs_cublas": [round(s, 3) for s in speedup],
             "cublas_ms": [round(c, 5) for c in cub],
@@ -478,6 +523,10 @@ def main(argv=None):
                     help="force a venom_spmm strategy (default: the library's cost model)")
     ap.add_argument("--form", choices=["auto", "vnm", "2to4"], default="auto",
                     help="SpMM operand form: V:N:M as compressed, or re-encoded V:2:4 (venom_expand_2to4)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time the eager step instead of its CUDA-graph replay")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false",
+                    help="run decompress after the SpMMs on the same stream instead of beside them")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

@@ -465,3 +465,39 @@ def test_spmm_full_size_bert_sampled(wl):
         y = venom.order_metadata(x)
     C = venom.spmm(y, Bd)
     check_spmm(C[:, torch.from_numpy(cols).cuda()], C_ref, F16)
+
+
+def test_step_under_cuda_graph_matches_eager():
+    """bench.py times the step as a CUDA graph replay: the captured launches (compress_2to4,
+    spmm with tensor-core metadata, decompress on a second stream) give bit-identical results."""
+    R, K, T, V, M = 512, 1024, 512, 64, 8
+    A = to_dev(synth.gaussian((R, K), 0.02, F16, 41), F16)
+    B = to_dev(synth.gaussian((K, T), 1.0, F16, 42), F16)
+    x, y = venom.compress_2to4(A, V=V, M=M, check=True)
+    C = torch.empty((R, T), dtype=torch.float16, device="cuda")
+    D = torch.empty((R, K), dtype=torch.float16, device="cuda")
+    side = torch.cuda.Stream()
+
+    def step():
+        venom.compress_2to4(A, V=V, M=M, out=(x, y))
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            venom.decompress(x, out=D)
+        venom.spmm(y, B, out=C)
+        torch.cuda.current_stream().wait_stream(side)
+    step()
+    torch.cuda.synchronize()
+    C_eager, D_eager = C.clone(), D.clone()
+    C.zero_()
+    D.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    C.zero_()
+    D.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C.view(torch.int16), C_eager.view(torch.int16))
+    assert torch.equal(D.view(torch.int16), D_eager.view(torch.int16))
+    parts = oracle.compress(to_bits(A), F16, V=V, M=M)
+    check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, to_bits(B)), F16)
