@@ -1,2 +1,4 @@
 python -m paper_2310_02065_b200.build >/dev/null
-timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+NOTEST=1 FORMS="auto" WLS="bert_large_ffn_4096tok_64:2:8 sweep_4096x4096x4096_64:2:4 sweep_4096x4096x4096_64:2:8 sweep_4096x4096x4096_64:2:16 sweep_4096x4096x4096_64:2:32 sweep_4096x4160x4096_64:2:40 sweep_4096x4096x4096_128:2:4 sweep_4096x4096x4096_128:2:8 sweep_4096x4096x4096_128:2:16 sweep_4096x4096x4096_128:2:32 sweep_4096x4160x4096_128:2:40 gpt3_ffn_12288x49152x8192_128:2:16" bash tools/quick_perf.sh > gpurun_out/sweep.txt 2>&1
+NOTEST=1 FORMS="vnm 2to4" WLS="sweep_4096x4096x4096_64:2:16 sweep_4096x4096x4096_64:2:32 sweep_4096x4096x4096_128:2:8 sweep_4096x4096x4096_128:2:16" bash tools/quick_perf.sh >> gpurun_out/sweep.txt 2>&1
+cat gpurun_out/sweep.txt
