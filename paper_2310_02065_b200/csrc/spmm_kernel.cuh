@@ -49,8 +49,10 @@ struct SpmmParams {
   int dbg;  // debug/ablation flags (0 in production)
 };
 
-template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8, int CG_ = 1, bool PRE_ = false>
+template <int NB_, int BN_, int STAGES_, int PRODUCERS_ = 8, int CG_ = 1, bool PRE_ = false, int MB_ = 1>
 struct SpmmCfg {
+  static constexpr int MB = MB_;              // 128-row blocks per CTA (2: two accumulators, one
+                                              // B tile serves both; CTA pair + 2:4 form only)
   static constexpr bool PRE = PRE_;           // metadata pre-ordered for the tensor core (TMA-loaded,
                                               // tcgen05.cp to TMEM by the MMA thread): no metadata warps
   static constexpr int NB = NB_;              // V-blocks per 128-row tile
@@ -62,31 +64,39 @@ struct SpmmCfg {
   static constexpr int P = PRODUCERS_;        // gather-issuing warps (TMA issue is per-warp serial)
   static constexpr int BM = 128;              // rows per CTA
   static constexpr int KG = 32;               // groups per k-stage: K' = 128, 4 MMAs of K = 32
-  static constexpr int A_BYTES = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
+  static constexpr int A_BLOCK = BM * 128;    // 128 rows × 64 compressed values × 2 B (SW128)
+  static constexpr int A_BYTES = MB_ * A_BLOCK;
   static constexpr int B_CHUNK = 128 * 128;   // 128 K'-rows × 64 columns × 2 B (SW128, MN-major)
-  static constexpr int B_BYTES = (BNH / 64) * B_CHUNK;
-  static constexpr int E_BYTES = PRE_ ? 128 * 16 : 0;  // 128 lanes × 4 metadata words
+  static constexpr int NCH = (BNH + 63) / 64; // 64-column chunks of B' per block (last may be partial)
+  static constexpr int B_BYTES = NCH * B_CHUNK;
+  static constexpr int E_BLOCK = 128 * 16;    // 128 lanes × 4 metadata words
+  static constexpr int E_BYTES = PRE_ ? MB_ * E_BLOCK : 0;
   static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES + E_BYTES;
   static constexpr int TX_BYTES = STAGE_BYTES;  // per CTA
-  static constexpr int ACC_COLS = NB * BN;
-  // TMEM: accumulators, then 4 metadata columns per stage (written by tcgen05.st)
-  static constexpr int ACC_BUFS = (2 * ACC_COLS + 4 * STAGES_ <= 512) ? 2 : 1;
+  static constexpr int ACC_COLS = NB * MB_ * BN;
+  // TMEM: accumulators, then 4 metadata columns per row block and stage
+  static constexpr int E_PER_STAGE = 4 * MB_;
+  static constexpr int ACC_BUFS = (2 * ACC_COLS + E_PER_STAGE * STAGES_ <= 512) ? 2 : 1;
   static constexpr int E_COL = ACC_BUFS * ACC_COLS;
-  static constexpr int NCH = BNH / 64;        // 64-column chunks of B' per block
   static constexpr int NOPS = NB * NCH * 32;  // gather4 ops per stage (one per group × chunk × block)
   static constexpr int OPS_PER_WARP = NOPS / P;
   static constexpr int LANE_OPS = (OPS_PER_WARP + 31) / 32;
   // warp roles: [0,P) producers, P MMA, P+1..P+8 epilogue, P+9..P+12 metadata; epilogue and
   // metadata warps address TMEM lane quarter (warp % 4)
-  static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 9, EPI_WARPS = 8;
-  static constexpr int NUM_THREADS = 32 * (P + (PRE_ ? 9 : 13));
+  // MB = 2: 16 epilogue warps (row block × column half × lane quarter) so that the whole
+  // accumulator pair fits in registers and is released before the stores
+  static constexpr int EPI_WARPS = (MB_ == 2) ? 16 : 8;
+  static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 1 + EPI_WARPS;
+  static constexpr int NUM_THREADS = 32 * (P + 1 + EPI_WARPS + (PRE_ ? 0 : 4));
   static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
   static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
   static constexpr int BAR_BYTES = 256;
-  static constexpr int EPI_STAGE_BYTES = 2048;  // per epilogue warp: 32 rows × 64 B output chunk
+  // per epilogue warp: one 32-row output chunk (64 B rows; 32 B rows for MB = 2)
+  static constexpr int EPI_STAGE_BYTES = (MB_ == 2) ? 1024 : 2048;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_WARPS * EPI_STAGE_BYTES;
-  static_assert(BNH % 64 == 0 && BN <= 256, "BN");
-  static_assert(E_COL + 4 * STAGES_ <= 512, "TMEM budget");
+  static_assert((BNH % 64 == 0 || MB_ == 2) && BNH % 8 == 0 && BN <= 256, "BN");
+  static_assert(MB_ == 1 || (CG_ == 2 && NB_ == 1 && PRE_), "two row blocks: CTA pair, pre-ordered metadata");
+  static_assert(E_COL + E_PER_STAGE * STAGES_ <= 512, "TMEM budget");
   static_assert(STAGE_BYTES % 1024 == 0, "stage alignment");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
@@ -170,26 +180,32 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
       if (lane == 0) VENOM_TRACE_EVENT(1, it);
       if (lane == 0 && !(p.dbg & 2)) {  // ablation 2: no MMAs (commits only)
         const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
-        const uint32_t e_tmem = tmem_base + Cfg::E_COL + 4 * stage;
+        const uint32_t e_tmem = tmem_base + Cfg::E_COL + Cfg::E_PER_STAGE * stage;
         if constexpr (Cfg::PRE) {
-          // pre-ordered metadata block of this stage: SMEM [128 lanes][16 B] -> 4 TMEM columns;
-          // tcgen05.cp and the MMAs below execute in issue order
-          const uint64_t edesc = smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES, 16, 128, 0);
-          if constexpr (CG == 2) tc_cp_128x128b_2sm(e_tmem, edesc);
-          else tc_cp_128x128b(e_tmem, edesc);
+          // pre-ordered metadata block(s) of this stage: SMEM [128 lanes][16 B] -> 4 TMEM columns
+          // per row block; tcgen05.cp and the MMAs below execute in issue order
+#pragma unroll
+          for (int mb = 0; mb < Cfg::MB; ++mb) {
+            const uint64_t edesc =
+                smem_desc(sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES + mb * Cfg::E_BLOCK, 16, 128, 0);
+            if constexpr (CG == 2) tc_cp_128x128b_2sm(e_tmem + 4 * mb, edesc);
+            else tc_cp_128x128b(e_tmem + 4 * mb, edesc);
+          }
         }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
-          const uint32_t e_addr = e_tmem + kb;
-          const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
-          // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
-          const uint64_t adesc = smem_desc(sbase + kb * 32, 16, 1024, 2);
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
+          for (int b = 0; b < NB * Cfg::MB; ++b) {
+            // MB = 2: row block b has its own A tile and metadata, the B tile is shared;
+            // NB > 1: V-block b has its own gathered B', the A tile is shared
+            const uint32_t e_addr = e_tmem + (Cfg::MB > 1 ? 4 * b : 0) + kb;
+            const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
+            // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
+            const uint64_t adesc = smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + kb * 32, 16, 1024, 2);
             // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
             // K advance 32 rows = 4096 B per MMA
-            const uint64_t bdesc =
-                smem_desc(sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + kb * 4096, Cfg::B_CHUNK, 1024, 2);
+            const uint64_t bdesc = smem_desc(sbase + Cfg::A_BYTES + (NB > 1 ? b * Cfg::B_BYTES : 0) + kb * 4096,
+                                             Cfg::B_CHUNK, 1024, 2);
             if constexpr (CG == 2)
               tc_mma_sp_f16_2sm(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
                                 (ks | kb) != 0 ? 1u : 0u);
@@ -310,6 +326,76 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
   }
 }
 
+// Epilogue for MB = 2 (two 128-row accumulators per CTA, BN = 240): 16 warps, warp e = w - W_EPI
+// takes row block e / 8, column half (e / 4) % 2 and TMEM lane quarter w % 4; its 32 × 120 slice
+// goes to registers (packed), the accumulator pair is released, then each 16-column chunk is
+// transposed through a 1 KB swizzled SMEM slot so a store writes 16 rows × 32 contiguous bytes.
+template <class Cfg, bool kBF16, int CG>
+__device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
+                                                  uint32_t accf0, uint32_t acce0, int warp, int lane,
+                                                  uint32_t stage_smem) {
+  using namespace ptx;
+  constexpr int BN = Cfg::BN;
+  constexpr int HALF = BN / 2;            // valid columns per half
+  constexpr int NCH = (HALF + 15) / 16;   // 16-column TMEM loads per half
+  const int e = warp - Cfg::W_EPI;
+  const int q = warp & 3;
+  const int b = e >> 3;
+  const int h = (e >> 2) & 1;
+  const uint32_t rank = cluster_ctarank();
+  for (int tl = 0; tl < my_tiles; ++tl) {
+    int m_tile, n_tile;
+    tile_coords<CG>(p, tl, m_tile, n_tile);
+    mbar_wait(accf0, tl & 1);
+    tc_fence_after();
+    const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG * 2) + b * (128 * CG) +
+                             128 * static_cast<int>(rank) + 32 * q;
+    const int64_t row = row_base + lane;
+    const float bv = (p.bias != nullptr && row < p.R)
+                         ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
+                                  : __half2float(__ushort_as_half(p.bias[row])))
+                         : 0.0f;
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + b * BN + h * HALF;
+    uint32_t pk[NCH][8];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(t_row + 16 * c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        pk[c][j] = pack2<kBF16>(__uint_as_float(v[2 * j]) + bv, __uint_as_float(v[2 * j + 1]) + bv);
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(mapa_shared(acce0, 0));  // pair leader
+    if (p.dbg & 4) continue;  // ablation 4: no C stores
+    const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HALF;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+      for (int sgm = 0; sgm < 2; ++sgm) {
+        const uint32_t a = stage_smem + lane * 32 + ((sgm ^ ((lane >> 2) & 1)) * 16);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c][4 * sgm]),
+                     "r"(pk[c][4 * sgm + 1]), "r"(pk[c][4 * sgm + 2]), "r"(pk[c][4 * sgm + 3]) : "memory");
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = 16 * j + (lane >> 1), sgm = lane & 1;
+        uint4 o;
+        const uint32_t a = stage_smem + r * 32 + ((sgm ^ ((r >> 2) & 1)) * 16);
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
+        const int64_t orow = row_base + r;
+        const int cc = 16 * c + 8 * sgm;  // column within the half
+        if (orow < p.R && cc < HALF && col_base + cc < p.T)
+          *reinterpret_cast<uint4*>(p.C + orow * p.ldc + col_base + cc) = o;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <class Cfg, bool kBF16>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
@@ -342,7 +428,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf0 + 8 * b, 1);           // (multicast) MMA commit
-      mbar_init(acce0 + 8 * b, 8 * CG);      // epilogue warps of the pair
+      mbar_init(acce0 + 8 * b, Cfg::EPI_WARPS * CG);  // epilogue warps of the pair
     }
     fence_mbar_init();
     prefetch_tmap(&tm_values);
@@ -419,7 +505,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
           const uint32_t fbar = (CG == 2) ? mapa_shared(full0 + 8 * stage, 0) : full0 + 8 * stage;
           const int col0 = n_tile * BN + static_cast<int>(rank) * Cfg::BNH;
-          const int arow = m_tile * 128 * CG + row_off;
+          const int arow = m_tile * 128 * CG * Cfg::MB + row_off;
           if (warp == 0 && lane == 0) {
             VENOM_TRACE_EVENT(0, it);
             // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load
@@ -427,16 +513,23 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
                                       (p.dbg & 2048 ? 0 : Cfg::E_BYTES));  // 2048: no metadata load
             if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
             if (!(p.dbg & 16)) {
-              if constexpr (CG == 2) tma_load_2d_2sm(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
-              else tma_load_2d(sbase, &tm_values, fbar, ks * 64, arow, pol_a);
+#pragma unroll
+              for (int mb = 0; mb < Cfg::MB; ++mb) {
+                const int ar = arow + mb * 128 * CG;
+                if constexpr (CG == 2) tma_load_2d_2sm(sbase + mb * Cfg::A_BLOCK, &tm_values, fbar, ks * 64, ar, pol_a);
+                else tma_load_2d(sbase + mb * Cfg::A_BLOCK, &tm_values, fbar, ks * 64, ar, pol_a);
+              }
             }
             if constexpr (Cfg::PRE) if (!(p.dbg & 2048)) {
-              // this CTA's 128-row tile, k-stage ks: row block (tile·num_ks + ks)·128 of the
+              // this CTA's 128-row tile(s), k-stage ks: row block (tile·num_ks + ks)·128 of the
               // [tiles·num_ks·128][4] u32 pre-ordered metadata
-              const uint32_t edst = sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES;
-              const int erow = ((m_tile * CG + static_cast<int>(rank)) * p.num_ks + ks) * 128;
-              if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, erow, pol_a);
-              else tma_load_2d(edst, &tm_e, fbar, 0, erow, pol_a);
+#pragma unroll
+              for (int mb = 0; mb < Cfg::MB; ++mb) {
+                const uint32_t edst = sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES + mb * Cfg::E_BLOCK;
+                const int erow = (((m_tile * Cfg::MB + mb) * CG + static_cast<int>(rank)) * p.num_ks + ks) * 128;
+                if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, erow, pol_a);
+                else tma_load_2d(edst, &tm_e, fbar, 0, erow, pol_a);
+              }
             }
           }
           if (contiguous && lane == 0 && !(p.dbg & 1)) {
@@ -479,10 +572,10 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     }
   } else if (warp == Cfg::W_MMA) {
     if (rank == 0) mma_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
-  } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + 8) {
-    epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane,
-                                  smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES +
-                                      (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES);
+  } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
+    const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
+    if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
+    else epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high

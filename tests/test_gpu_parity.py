@@ -501,3 +501,36 @@ def test_step_under_cuda_graph_matches_eager():
     assert torch.equal(D.view(torch.int16), D_eager.view(torch.int16))
     parts = oracle.compress(to_bits(A), F16, V=V, M=M)
     check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, to_bits(B)), F16)
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,bias", [
+    (640, 512, 520, 64, 4, F16, True),      # ragged 512-row tile, ragged 240-column tile
+    (1024, 1024, 480, 128, 4, BF16, False),
+    (512, 2048, 240, 32, 4, F16, True),
+    (1536, 256, 1000, 16, 4, F16, False),   # short K (2 k-stages), several tiles per CTA pair
+])
+def test_spmm_two_row_blocks_per_cta(R, K, T, V, M, dt, bias):
+    """tile_t = 240: 512 × 240 CTA-pair tiles with two accumulators per CTA."""
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 800 + R + K + T, bias)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = venom.order_metadata(vnm_from(parts, R, K, V, M, dt))
+    C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=240)
+    check_spmm(C, C_ref, dt)
+
+
+def test_spmm_two_row_blocks_identity_and_2to4_form():
+    """B = I through the 512 × 240 tiles is exact; and the fused V:2:4 form of a 64:2:8 matrix."""
+    R, K, V, M = 768, 512, 64, 4
+    A = synth.gaussian((R, K), 1.0, F16, 83)
+    parts = oracle.compress(A, F16, V=V, M=M)
+    D = oracle.decompress(*parts, R, K, F16, V, M)
+    x = venom.order_metadata(vnm_from(parts, R, K, V, M, F16))
+    C = venom.spmm(x, to_dev(f64_to_bits(np.eye(K), F16), F16), tile_t=240)
+    assert np.array_equal(bits_to_f64(to_bits(C), F16), bits_to_f64(D, F16))
+    R, K, T, V, M = 1024, 1024, 960, 64, 8
+    A = synth.gaussian((R, K), 0.02, F16, 84)
+    B = synth.gaussian((K, T), 1.0, F16, 85)
+    _, y = venom.compress_2to4(to_dev(A, F16), V=V, M=M, check=True)
+    C = venom.spmm(y, to_dev(B, F16), tile_t=240)
+    parts = oracle.compress(A, F16, V=V, M=M)
+    check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, B), F16)

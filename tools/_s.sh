@@ -1,4 +1,8 @@
 python -m paper_2310_02065_b200.build >/dev/null
-NOTEST=1 FORMS="auto" WLS="bert_large_ffn_4096tok_64:2:8 sweep_4096x4096x4096_64:2:4 sweep_4096x4096x4096_64:2:8 sweep_4096x4096x4096_64:2:16 sweep_4096x4096x4096_64:2:32 sweep_4096x4160x4096_64:2:40 sweep_4096x4096x4096_128:2:4 sweep_4096x4096x4096_128:2:8 sweep_4096x4096x4096_128:2:16 sweep_4096x4096x4096_128:2:32 sweep_4096x4160x4096_128:2:40 gpt3_ffn_12288x49152x8192_128:2:16" bash tools/quick_perf.sh > gpurun_out/sweep.txt 2>&1
-NOTEST=1 FORMS="vnm 2to4" WLS="sweep_4096x4096x4096_64:2:16 sweep_4096x4096x4096_64:2:32 sweep_4096x4096x4096_128:2:8 sweep_4096x4096x4096_128:2:16" bash tools/quick_perf.sh >> gpurun_out/sweep.txt 2>&1
-cat gpurun_out/sweep.txt
+timeout 600 python -m pytest tests -q -m gpu -x -k "two_row" > gpurun_out/pytest_gpu.txt 2>&1; tail -3 gpurun_out/pytest_gpu.txt
+for t in 256 240; do
+TILE=$t timeout 60 python tools/ablate.py 1024 4096 4096 64 4 1 2 0 4 | grep -v host
+TILE=$t timeout 60 python tools/ablate.py 4096 1024 4096 64 4 1 2 0 4 | grep -v host
+TILE=$t timeout 60 python tools/ablate.py 4096 4096 4096 128 4 1 2 0 4 | grep -v host
+TILE=$t timeout 60 python tools/ablate.py 4096 8192 8192 128 4 1 2 0 | grep -v host
+done

@@ -9,6 +9,7 @@ import paper_2310_02065_b200 as venom
 R, K, T, V, M, strat, pair = (int(x) for x in sys.argv[1:8])
 flags = [int(x) for x in sys.argv[8:]] or [0]
 prepared = os.environ.get("PREPARED", "1") == "1"
+tile = int(os.environ.get("TILE", "0"))
 torch.manual_seed(0)
 A = (torch.randn(R, K, device="cuda") * 0.02).half()
 B = torch.randn(K, T, device="cuda").half()
@@ -25,12 +26,12 @@ for fl in flags:
         torch.cuda._sleep(200000)  # ~100 us: the host enqueues the launch before the GPU gets there
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        venom.spmm(x, B, out=C, strategy=strat, cta_pair=pair)
+        venom.spmm(x, B, out=C, strategy=strat, cta_pair=pair, tile_t=tile)
         b.record()
         ts.append((a, b))
     torch.cuda.synchronize()
     ms = statistics.median(a.elapsed_time(b) for a, b in ts[2:])
-    print(f"R{R} K{K} T{T} V{V} M{M} strat{strat} pair{pair} flags {fl:3d}: {ms*1e3:8.1f} us "
+    print(f"R{R} K{K} T{T} V{V} M{M} strat{strat} pair{pair} tile{tile} flags {fl:3d}: {ms*1e3:8.1f} us "
           f"{4*R*K*T/M/ms/1e9:7.1f} TF/s")
 os.environ["VENOM_DEBUG_FLAGS"] = "0"
 # host-side cost of one call (enqueue only)
