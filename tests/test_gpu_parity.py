@@ -534,3 +534,20 @@ def test_spmm_two_row_blocks_identity_and_2to4_form():
     C = venom.spmm(y, to_dev(B, F16), tile_t=240)
     parts = oracle.compress(A, F16, V=V, M=M)
     check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, B), F16)
+
+
+def test_sparse_encoder_matches_dense_on_pruned_weights():
+    """§8(f) rank 1: two BERT-large encoder layers with every linear layer 64:2:10 through
+    venom_spmm equal the same encoder with torch fp32 GEMMs on the decompressed weights."""
+    from paper_2310_02065_b200 import encoder as enc
+    cfg = enc.EncoderConfig(layers=2, batch=2, seq=128)
+    W = enc.init_weights(cfg, torch.device("cuda"), seed=3)
+    model = enc.SparseEncoder(cfg, W)
+    dense = model.dense_weights()
+    x = (torch.randn(cfg.tokens, cfg.hidden, generator=torch.Generator().manual_seed(5))).half().cuda()
+    ys = model.forward(x).float()
+    d32 = [{k: (tuple(t.float() for t in v) if isinstance(v, tuple) else v.float()) for k, v in L.items()}
+           for L in dense]
+    yd = enc.dense_forward(cfg, d32, x.float())
+    rel = float((ys - yd).norm() / yd.norm())
+    assert rel <= 1e-2, rel

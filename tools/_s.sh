@@ -1,8 +1,15 @@
 python -m paper_2310_02065_b200.build >/dev/null
-timeout 600 python -m pytest tests -q -m gpu -x -k "two_row" > gpurun_out/pytest_gpu.txt 2>&1; tail -3 gpurun_out/pytest_gpu.txt
-for t in 256 240; do
-TILE=$t timeout 60 python tools/ablate.py 1024 4096 4096 64 4 1 2 0 4 | grep -v host
-TILE=$t timeout 60 python tools/ablate.py 4096 1024 4096 64 4 1 2 0 4 | grep -v host
-TILE=$t timeout 60 python tools/ablate.py 4096 4096 4096 128 4 1 2 0 4 | grep -v host
-TILE=$t timeout 60 python tools/ablate.py 4096 8192 8192 128 4 1 2 0 | grep -v host
+for shape in "3072 1040" "1024 1040" "4096 1040" "1024 4160"; do
+  timeout 60 python tools/ablate.py $shape 16384 64 10 0 0 0 | grep -v host
 done
+timeout 120 python -c "
+import torch,statistics
+for (R,K) in [(3072,1024),(1024,1024),(4096,1024),(1024,4096)]:
+    W=torch.randn(R,K,device='cuda').half(); X=torch.randn(16384,K,device='cuda').half()
+    for _ in range(3): torch.matmul(X,W.t())
+    torch.cuda.synchronize()
+    ts=[]
+    for _ in range(10):
+        a,b=torch.cuda.Event(enable_timing=True),torch.cuda.Event(enable_timing=True); a.record(); torch.matmul(X,W.t()); b.record(); ts.append((a,b))
+    torch.cuda.synchronize(); print('dense',R,K,statistics.median(a.elapsed_time(b) for a,b in ts)*1e3,'us')
+"
