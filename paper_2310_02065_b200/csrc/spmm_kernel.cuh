@@ -337,7 +337,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
   using namespace ptx;
   constexpr int BN = Cfg::BN;
   constexpr int HALF = BN / 2;            // valid columns per half
-  constexpr int NCH = (HALF + 15) / 16;   // 16-column TMEM loads per half
+  constexpr int NCH = 2 * ((HALF + 31) / 32);  // 16-column TMEM loads per half (even)
   const int e = warp - Cfg::W_EPI;
   const int q = warp & 3;
   const int b = e >> 3;
@@ -371,27 +371,36 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
     if (lane == 0) mbar_arrive_cluster(mapa_shared(acce0, 0));  // pair leader
     if (p.dbg & 4) continue;  // ablation 4: no C stores
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HALF;
+    // 32-column chunks (64 B per row), 16 rows at a time through the 1 KB slot: every store
+    // instruction writes 8 rows × 64 contiguous bytes
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NCH / 2; ++c) {
 #pragma unroll
-      for (int sgm = 0; sgm < 2; ++sgm) {
-        const uint32_t a = stage_smem + lane * 32 + ((sgm ^ ((lane >> 2) & 1)) * 16);
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c][4 * sgm]),
-                     "r"(pk[c][4 * sgm + 1]), "r"(pk[c][4 * sgm + 2]), "r"(pk[c][4 * sgm + 3]) : "memory");
+      for (int hh = 0; hh < 2; ++hh) {
+        if ((lane >> 4) == hh) {
+          const int rr = lane & 15;
+#pragma unroll
+          for (int sgm = 0; sgm < 4; ++sgm) {
+            const uint32_t* src = pk[2 * c + (sgm >> 1)] + 4 * (sgm & 1);
+            const uint32_t a = stage_smem + rr * 64 + ((sgm ^ ((rr >> 1) & 3)) * 16);
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(src[0]), "r"(src[1]),
+                         "r"(src[2]), "r"(src[3]) : "memory");
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = 8 * j + (lane >> 2), sgm = lane & 3;
+          uint4 o;
+          const uint32_t a = stage_smem + r * 64 + ((sgm ^ ((r >> 1) & 3)) * 16);
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
+          const int64_t orow = row_base + 16 * hh + r;
+          const int cc = 32 * c + 8 * sgm;  // column within the half
+          if (orow < p.R && cc < HALF && col_base + cc < p.T)
+            *reinterpret_cast<uint4*>(p.C + orow * p.ldc + col_base + cc) = o;
+        }
+        __syncwarp();
       }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int r = 16 * j + (lane >> 1), sgm = lane & 1;
-        uint4 o;
-        const uint32_t a = stage_smem + r * 32 + ((sgm ^ ((r >> 2) & 1)) * 16);
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
-        const int64_t orow = row_base + r;
-        const int cc = 16 * c + 8 * sgm;  // column within the half
-        if (orow < p.R && cc < HALF && col_base + cc < p.T)
-          *reinterpret_cast<uint4*>(p.C + orow * p.ldc + col_base + cc) = o;
-      }
-      __syncwarp();
     }
   }
 }

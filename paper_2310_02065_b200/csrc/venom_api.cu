@@ -577,7 +577,19 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   const bool pair_ok = NBg == 1 && (contiguous || V % 256 == 0);
   const int pair = (opts && opts->cta_pair) ? opts->cta_pair : (pair_ok ? 2 : 1);
   if (pair == 2 && !pair_ok) return VENOM_ERR_INVALID_ARGUMENT;
-  if (tile_t == 0) tile_t = (NBg == 1) ? 256 : (NBg == 2 ? 128 : 64);
+  if (tile_t == 0) {
+    tile_t = (NBg == 1) ? 256 : (NBg == 2 ? 128 : 64);
+    // 512 × 240 pair tiles (two accumulators per CTA) land 1.45× fewer bytes per FLOP but expose a
+    // larger last epilogue: measured better only with long k-loops and at least one full wave of
+    // pair tiles
+    if (contiguous && pair == 2 && opts && opts->metadata_tc) {
+      int sms = 148, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t tiles240 = ((R + 511) / 512) * ((T + 239) / 240);
+      if (p.num_ks >= 24 && tiles240 >= sms / 2) tile_t = 240;
+    }
+  }
   set_tiles(tile_t);
   (void)stages;
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
