@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
   if (bad && status != nullptr) atomicMax(status, kStatusNonFinite);
   __syncthreads();
 
-  // ---- phase 1: column L1 mass, fp64, ascending rows
+  // ---- phase 1: column L1 mass
   for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
     double acc = 0.0;
     if (dbg & 2) {
@@ -370,23 +370,33 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
         v[t] = trow[(cw >> (8 * t)) & 0xFFu];
         mag[t] = v[t] & 0x7FFFu;  // |w| order for finite sign-magnitude formats; ±0 tie
       }
+      // top-2 by (|a| desc, position asc) with register-only selects (no local-memory indexing)
       int p0 = 0;
+      uint32_t m0 = mag[0];
 #pragma unroll
       for (int t = 1; t < 4; ++t)
-        if (mag[t] > mag[p0]) p0 = t;
+        if (mag[t] > m0) { p0 = t; m0 = mag[t]; }
       int p1 = -1;
+      uint32_t m1 = 0;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (t != p0 && (p1 < 0 || mag[t] > mag[p1])) p1 = t;
+        if (t != p0 && (p1 < 0 || mag[t] > m1)) { p1 = t; m1 = mag[t]; }
       const int lo = min(p0, p1), hi = max(p0, p1);
+      uint16_t vlo = v[0], vhi = v[0];
+#pragma unroll
+      for (int t = 1; t < 4; ++t) {
+        if (t == lo) vlo = v[t];
+        if (t == hi) vhi = v[t];
+      }
       nibble = static_cast<uint32_t>(lo | (hi << 2));
       reinterpret_cast<uint32_t*>(values)[row * G + g0 + q] =
-          static_cast<uint32_t>(v[lo]) | (static_cast<uint32_t>(v[hi]) << 16);
+          static_cast<uint32_t>(vlo) | (static_cast<uint32_t>(vhi) << 16);
       if constexpr (kExpand) {
         // the same matrix as V:2:4 over the original K (reading #18): per 4-column
         // subgroup the kept values (inserted zeros +0.0) and one nibble; M % 8 == 0, so the
         // group's subgroups fill whole bytes of s_m2
         const int ca = static_cast<int>((cw >> (8 * lo)) & 0xFFu), cb = static_cast<int>((cw >> (8 * hi)) & 0xFFu);
+        const uint32_t va = vlo, vb = vhi;
         const int sub = M / 4;
         uint32_t* v2 = values2 + row * (K / 4) + (g0 + q) * sub;
         uint32_t nbits = 0;
@@ -395,10 +405,10 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
           const bool in0 = (ca >= j0 && ca < j0 + 4), in1 = (cb >= j0 && cb < j0 + 4);
           uint32_t wv, nb;
           if (in0 && in1) {
-            wv = static_cast<uint32_t>(v[lo]) | (static_cast<uint32_t>(v[hi]) << 16);
+            wv = va | (vb << 16);
             nb = static_cast<uint32_t>(ca - j0) | (static_cast<uint32_t>(cb - j0) << 2);
           } else if (in0 || in1) {
-            const uint32_t x = in0 ? v[lo] : v[hi];
+            const uint32_t x = in0 ? va : vb;
             const uint32_t ii = static_cast<uint32_t>((in0 ? ca : cb) - j0);
             wv = (ii == 0u) ? x : (x << 16);
             nb = (ii == 0u) ? 0x4u : (ii << 2);
