@@ -30,6 +30,12 @@ WORKLOADS = {
     "sweep_4096x4096x4096_64:2:16": dict(R=4096, K=4096, T=4096, V=64, M=16, cfg=2),
     "sweep_4096x4096x4096_64:2:32": dict(R=4096, K=4096, T=4096, V=64, M=32, cfg=2),
     "sweep_4096x4160x4096_64:2:40": dict(R=4096, K=4160, T=4096, V=64, M=40, cfg=2),
+    # the paper's Fig 6 family: BERT-large-shaped 1024×K×4096 at V = 128,
+    # N:M = 2:10 / 2:20 / 2:40 / 2:100 (K padded to a multiple of 8M, reading #11)
+    "fig6_1024x4160x4096_128:2:10": dict(R=1024, K=4160, T=4096, V=128, M=10, cfg=1),
+    "fig6_1024x4160x4096_128:2:20": dict(R=1024, K=4160, T=4096, V=128, M=20, cfg=1),
+    "fig6_1024x4160x4096_128:2:40": dict(R=1024, K=4160, T=4096, V=128, M=40, cfg=1),
+    "fig6_1024x4800x4096_128:2:100": dict(R=1024, K=4800, T=4096, V=128, M=100, cfg=1),
     "gpt3_ffn_12288x49152x8192_128:2:16": dict(R=12288, K=49152, T=8192, V=128, M=16, cfg=3),
 }
 

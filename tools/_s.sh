@@ -1,3 +1,2 @@
 python -m paper_2310_02065_b200.build >/dev/null
-timeout 900 python -m pytest tests -q -m gpu -x -k "compress or encoder or graph" > gpurun_out/pytest_gpu.txt 2>&1; tail -2 gpurun_out/pytest_gpu.txt
-bash tools/ncu_times.sh gpurun_out/t1.csv python tools/time_format.py | grep venom
+NOTEST=1 FORMS="auto" WLS="fig6_1024x4160x4096_128:2:10 fig6_1024x4160x4096_128:2:20 fig6_1024x4160x4096_128:2:40 fig6_1024x4800x4096_128:2:100" bash tools/quick_perf.sh > gpurun_out/fig6.txt 2>&1; cat gpurun_out/fig6.txt
