@@ -41,7 +41,7 @@ def full(rep, out, key=None):
     lines += ["", "| kernel | duration us | DRAM GB/s | % of HBM peak (6549.4 GB/s, MEASURED_PEAKS.json) | "
               "L2->SMEM GB/s | tensor pipe active % |", "|---|---|---|---|---|---|"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1.0}
+             "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
     for r in data:
         d = dict(zip(hdr, r)); uu = dict(zip(hdr, units))
         try:
@@ -87,7 +87,7 @@ def launches(csvf, out):
     lines += ["", "| kernel | duration us | DRAM GB/s | % of HBM peak (6549.4 GB/s, MEASURED_PEAKS.json) | "
               "L2->SMEM GB/s | tensor pipe active % |", "|---|---|---|---|---|---|"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1.0}
+             "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
     for r in data:
         d = dict(zip(hdr, r)); uu = dict(zip(hdr, units))
         try:
