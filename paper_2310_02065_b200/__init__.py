@@ -20,7 +20,8 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvenom.so")
+# VENOM_LIB selects another build of the same ABI (tools/ablate.py: libvenom_ablation.so)
+LIB_PATH = os.environ.get("VENOM_LIB") or os.path.join(_HERE, "libvenom.so")
 
 OK = 0
 STATUS_NAMES = {

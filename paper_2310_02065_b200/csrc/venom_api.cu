@@ -60,10 +60,15 @@ bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p
 
 constexpr int kCompressThreads = 512;
 
-// ablation / debug flags for tools (VENOM_DEBUG_FLAGS; 0 in production)
+// ablation flags for the analysis tools (VENOM_DEBUG_FLAGS): honoured only by the separate
+// -DVENOM_ABLATION build (libvenom_ablation.so); the production library always passes 0
 int debug_flags() {
+#ifdef VENOM_ABLATION
   const char* d = getenv("VENOM_DEBUG_FLAGS");
   return d ? atoi(d) : 0;
+#else
+  return 0;
+#endif
 }
 
 venom_status_t launch_status() {
@@ -517,10 +522,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.meta_row = static_cast<int>((G + 1) / 2);
   p.m_tiles = static_cast<int>((R + 127) / 128);
   p.is_bf16 = bf16;
-  {
-    const char* d = getenv("VENOM_DEBUG_FLAGS");
-    p.dbg = d ? atoi(d) : 0;
-  }
+  p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
     p.num_tiles = p.m_tiles * p.n_tiles;
