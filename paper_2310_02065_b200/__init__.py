@@ -20,8 +20,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# VENOM_LIB selects another build of the same ABI (tools/ablate.py: libvenom_ablation.so)
-LIB_PATH = os.environ.get("VENOM_LIB") or os.path.join(_HERE, "libvenom.so")
+LIB_PATH = os.path.join(_HERE, "libvenom.so")
 
 OK = 0
 STATUS_NAMES = {
@@ -63,10 +62,12 @@ def lib() -> ctypes.CDLL:
     """Load libvenom.so (built by ``build()`` / ``__graft_entry__.build()``); raise if absent."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"libvenom.so not built ({LIB_PATH}); run python -m "
+        # VENOM_LIB selects another build of the same ABI (tools/ablate.py: libvenom_ablation.so)
+        path = os.environ.get("VENOM_LIB") or LIB_PATH
+        if not os.path.exists(path):
+            raise RuntimeError(f"libvenom.so not built ({path}); run python -m "
                                "paper_2310_02065_b200.build — there is no CPU fallback")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
         L.venom_compressed_sizes.argtypes = [I64, I64, _Format, P, P, P]
         L.venom_compress.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P]

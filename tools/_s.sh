@@ -1,2 +1,4 @@
 python -m paper_2310_02065_b200.build >/dev/null
-NOTEST=1 FORMS="auto" WLS="fig6_1024x4160x4096_128:2:10 fig6_1024x4160x4096_128:2:20 fig6_1024x4160x4096_128:2:40 fig6_1024x4800x4096_128:2:100" bash tools/quick_perf.sh > gpurun_out/fig6.txt 2>&1; cat gpurun_out/fig6.txt
+timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1; tail -2 gpurun_out/pytest_gpu.txt
+VENOM_DEBUG_FLAGS=4 timeout 300 python bench.py --no-cpu-baseline --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', d['value'], d['spmm_only'])"
+timeout 120 python tools/ablate.py 4096 1024 4096 64 4 1 2 0 4 | grep -v host
