@@ -163,10 +163,13 @@ venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t 
 int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f);
 
 /* Optional overrides for venom_spmm (benchmarking / tuning / ablation). Zero = library default.
- *   tile_t    output columns per CTA tile (64, 128, 192 or 256; availability depends on strategy)
+ *   tile_t    output columns per CTA tile (64, 128, 192 or 256; availability depends on strategy;
+ *             240 = 512 × 240 CTA-pair tiles with two accumulators per CTA, M == 4 operands with
+ *             metadata_tc only. 0 = the planner's choice)
  *   stages    pipeline depth (where a variant exists)
  *   max_ctas  persistent grid cap (0 = #SMs)
- *   strategy  VENOM_STRATEGY_AUTO: cost model; GATHER: the paper's mapping (gather the 4 selected
+ *   strategy  VENOM_STRATEGY_AUTO: the gathered/contiguous kernel wherever it applies, else
+ *             DENSE_K; GATHER: the paper's mapping (gather the 4 selected
  *             B rows per group through column_idx, 2:4 MMA over K' = 4K/M); DENSE_K: expand the
  *             V:N:M operand on the fly to 2:4 over the original K and use dense B tiles (requires
  *             M in {4,8,16,32}, G % 4 == 0). Both return the same product. */
