@@ -83,23 +83,6 @@ def launches(csvf, out):
              "| kernel | launches | total ns | share |", "|---|---|---|---|"]
     for n, t in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"| {n} | {cnt[n]} | {t:.0f} | {t / allt:.3f} |")
-    # derived: achieved HBM GB/s against the measured peak, L2->SMEM feed, sparse tensor-pipe use
-    lines += ["", "| kernel | duration us | DRAM GB/s | % of HBM peak (6549.4 GB/s, MEASURED_PEAKS.json) | "
-              "L2->SMEM GB/s | tensor pipe active % |", "|---|---|---|---|---|---|"]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
-    for r in data:
-        d = dict(zip(hdr, r)); uu = dict(zip(hdr, units))
-        try:
-            t = float(d["gpu__time_duration.sum"]) * scale.get(uu["gpu__time_duration.sum"], 1e-6)
-            db = float(d["dram__bytes_read.sum"]) * scale.get(uu["dram__bytes_read.sum"], 1) + \
-                float(d["dram__bytes_write.sum"]) * scale.get(uu["dram__bytes_write.sum"], 1)
-            xb = float(d["l1tex__m_xbar2l1tex_read_bytes.sum"]) * scale.get(uu["l1tex__m_xbar2l1tex_read_bytes.sum"], 1)
-            tp = d.get("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active", "-")
-            lines.append(f"| {d.get('Kernel Name', '?')[:60]} | {t * 1e6:.2f} | {db / t / 1e9:.0f} | "
-                         f"{db / t / 1e9 / 6549.4 * 100:.1f} | {xb / t / 1e9:.0f} | {tp} |")
-        except Exception:
-            pass
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
