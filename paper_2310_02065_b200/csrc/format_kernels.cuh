@@ -283,32 +283,38 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
   __syncthreads();
 
   // ---- phase 1: column L1 mass
-  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-    double acc = 0.0;
-    if (dbg & 2) {
-    } else if constexpr (!kBF16) {
-      // fp16: |a| = k·2^-24 with integer k < 2^40, so the column sum is an exact integer (< 2^53
-      // for V <= 8192): accumulate k in 64-bit integers (any order, 4 independent chains) and
-      // convert once — the same value as the oracle's sequential fp64 sum (reading #2)
-      uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-      auto kval = [](uint16_t bb) -> uint64_t {
-        const uint32_t e = (bb >> 10) & 0x1Fu, f = bb & 0x3FFu;
-        return e == 0 ? static_cast<uint64_t>(f) : (static_cast<uint64_t>(1024u + f) << (e - 1));
-      };
-      int i = 0;
-      for (; i + 4 <= V; i += 4) {
-        s0 += kval(tile[(i + 0) * W + c]);
-        s1 += kval(tile[(i + 1) * W + c]);
-        s2 += kval(tile[(i + 2) * W + c]);
-        s3 += kval(tile[(i + 3) * W + c]);
+  if constexpr (!kBF16) {
+    // fp16: every |a| is k·2^-24 with integer k < 2^40 and the column sums stay < 2^53, so fp64
+    // addition is exact in any order — the oracle's sequential sum bit for bit (reading #2). Two
+    // threads per column (row halves, 4 independent chains each); the halves meet in shared memory.
+    double* s_half = reinterpret_cast<double*>(s_m2 + (kExpand ? V * (W / 8) : 0));
+    s_half = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_half) + 15) & ~uintptr_t(15));
+    for (int t = threadIdx.x; t < 2 * ncols; t += blockDim.x) {
+      const int c = t % ncols, hf = t / ncols;
+      const int r0 = hf * (V / 2), r1 = hf ? V : V / 2;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (!(dbg & 2)) {
+        int i = r0;
+        for (; i + 4 <= r1; i += 4) {
+          a0 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 0) * W + c])));
+          a1 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 1) * W + c])));
+          a2 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 2) * W + c])));
+          a3 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 3) * W + c])));
+        }
+        for (; i < r1; ++i) a0 += static_cast<double>(fabsf(bits_to_float<false>(tile[i * W + c])));
       }
-      for (; i < V; ++i) s0 += kval(tile[i * W + c]);
-      acc = ldexp(static_cast<double>(s0 + s1 + s2 + s3), -24);
-    } else {
-      // bf16: not exact in general — the oracle's order (ascending rows, fp64)
-      for (int i = 0; i < V; ++i) acc = __dadd_rn(acc, static_cast<double>(fabsf(bits_to_float<kBF16>(tile[i * W + c]))));
+      s_half[hf * W + c] = (a0 + a1) + (a2 + a3);
     }
-    s_score[c] = acc;
+    __syncthreads();
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) s_score[c] = s_half[c] + s_half[W + c];
+  } else {
+    // bf16: not exact in general — the oracle's order (ascending rows, fp64), one thread per column
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+      double acc = 0.0;
+      if (!(dbg & 2))
+        for (int i = 0; i < V; ++i) acc = __dadd_rn(acc, static_cast<double>(fabsf(bits_to_float<true>(tile[i * W + c]))));
+      s_score[c] = acc;
+    }
   }
   __syncthreads();
 

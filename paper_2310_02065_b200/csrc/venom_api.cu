@@ -287,7 +287,8 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
            (gt / 2) % 2 == 0)
       gt /= 2;
     const size_t tsmem = ((static_cast<size_t>(f.v) * gt * f.m * 2 + 15) & ~size_t(15)) +
-                         8 * static_cast<size_t>(gt) * f.m + 4 * static_cast<size_t>(gt);
+                         8 * static_cast<size_t>(gt) * f.m + 4 * static_cast<size_t>(gt) + 16 +
+                         16 * static_cast<size_t>(gt) * f.m;  // + fp16 row-half partial sums
     if (tsmem <= 100 * 1024 && (R / f.v) <= 65535) {
       const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
       auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, false>
@@ -353,7 +354,8 @@ venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t 
   const int gt = W / f.m > 0 ? W / f.m : 1;
   if (gt * f.m != W) return VENOM_ERR_UNSUPPORTED_PATTERN;  // M must divide W (M | 128)
   const size_t tsmem = ((static_cast<size_t>(f.v) * W * 2 + 15) & ~size_t(15)) + 8 * static_cast<size_t>(W) +
-                       4 * static_cast<size_t>(gt) + static_cast<size_t>(f.v) * (W / 8);
+                       4 * static_cast<size_t>(gt) + static_cast<size_t>(f.v) * (W / 8) + 16 +
+                       16 * static_cast<size_t>(W);  // + fp16 row-half partial sums
   const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
   auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, true>
                                  : venom::vnm_compress_tile_kernel<false, true>;

@@ -1,5 +1,4 @@
 python -m paper_2310_02065_b200.build >/dev/null
-timeout 60 python tools/ablate.py 4096 2048 4096 128 4 1 2 0 | grep -v host
-timeout 60 python tools/ablate.py 4096 4096 4096 128 8 1 1 0 | grep -v host
-timeout 60 python tools/ablate.py 4096 1024 4096 128 4 1 2 0 | grep -v host
-timeout 60 python tools/ablate.py 4096 4096 4096 128 16 1 1 0 | grep -v host
+timeout 900 python -m pytest tests -q -m gpu -x -k "compress" > gpurun_out/pytest_gpu.txt 2>&1; tail -2 gpurun_out/pytest_gpu.txt
+python -m paper_2310_02065_b200.build --ablation >/dev/null
+for fl in 0 2; do echo "flags $fl: $(VENOM_DEBUG_FLAGS=$fl bash tools/ncu_times.sh gpurun_out/t2.csv python tools/time_format.py 2>&1 | grep 'compress_tile_kernel')"; done
