@@ -46,6 +46,7 @@ struct SpmmParams {
   int n_tiles;   // ceil(T / BN)
   int num_tiles;
   int is_bf16;
+  int b3d;  // M = 4: B map is 3-D [T/64][K][64] (one box per stage) instead of 2-D
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -530,20 +531,27 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
               }
             }
             if constexpr (Cfg::PRE) if (!(p.dbg & 2048)) {
-              // this CTA's 128-row tile(s), k-stage ks: row block (tile·num_ks + ks)·128 of the
-              // [tiles·num_ks·128][4] u32 pre-ordered metadata
+              // this CTA's 128-row tile(s), k-stage ks: 2 KB block (tile·num_ks + ks) of the
+              // pre-ordered metadata, one TMA row
 #pragma unroll
               for (int mb = 0; mb < Cfg::MB; ++mb) {
                 const uint32_t edst = sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES + mb * Cfg::E_BLOCK;
-                const int erow = (((m_tile * Cfg::MB + mb) * CG + static_cast<int>(rank)) * p.num_ks + ks) * 128;
-                if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, erow, pol_a);
-                else tma_load_2d(edst, &tm_e, fbar, 0, erow, pol_a);
+                const int eblk = ((m_tile * Cfg::MB + mb) * CG + static_cast<int>(rank)) * p.num_ks + ks;
+                if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, eblk, pol_a);
+                else tma_load_2d(edst, &tm_e, fbar, 0, eblk, pol_a);
               }
             }
           }
-          if (contiguous && lane == 0 && !(p.dbg & 1)) {
-            // M = 4: the 4 "selected" rows of every group are the group itself — plain tile boxes,
-            // one per 64-column chunk, issued by different warps (TMA issue is per-warp serial)
+          if (contiguous && p.b3d && warp == 1 && lane == 0 && !(p.dbg & 1)) {
+            // M = 4: the 4 "selected" rows of every group are the group itself, so B' is a plain
+            // K-slice of B: one 3-D box [NCH chunks][128 rows][64 columns] per stage (every TMA op
+            // costs the issuing warp a fixed overhead, so fewer, larger ops land faster)
+            const uint32_t bdst = sbase + Cfg::A_BYTES;
+            if constexpr (CG == 2) tma_load_3d_2sm(bdst, &tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
+            else tma_load_3d(bdst, &tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
+          }
+          if (contiguous && !p.b3d && lane == 0 && !(p.dbg & 1)) {
+            // M = 4 with T % 64 != 0: 2-D boxes, one per 64-column chunk, on different warps
 #pragma unroll
             for (int b = 0; b < NB; ++b)
 #pragma unroll

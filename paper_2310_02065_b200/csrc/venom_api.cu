@@ -524,6 +524,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.meta_row = static_cast<int>((G + 1) / 2);
   p.m_tiles = static_cast<int>((R + 127) / 128);
   p.is_bf16 = bf16;
+  p.b3d = 0;
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -573,9 +574,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
       return VENOM_ERR_CUDA;
   }
   // B: 2-D [K rows][T] 16-bit, 128B swizzle; box 64 × 1 row for gather4 (4 rows per op), or
-  // 64 × 128 rows when M = 4 (every group's 4 columns are selected: plain K-slices of B)
+  // 64 × 128 rows when M = 4 (every group's 4 columns are selected: plain K-slices of B). With
+  // T % 64 == 0 the M = 4 map is 3-D [T/64 chunks][K rows][64 columns] (chunk stride 128 B) so one
+  // box [NCH][128][64] lands the CTA's whole B' stage in the chunked SW128 layout.
   const bool contiguous = (f.m == 4);
-  if (!encode_b(&tb, contiguous ? 128 : 1)) return VENOM_ERR_CUDA;
   p.num_ks = static_cast<int>((G + 31) / 32);
   const int NBg = contiguous ? 1 : NB;  // M = 4 ignores V (column_idx is the identity)
   const bool pair_ok = NBg == 1 && (contiguous || V % 256 == 0);
@@ -596,18 +598,33 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   }
   set_tiles(tile_t);
   (void)stages;
+  p.b3d = contiguous && (T % 64 == 0) && ((tile_t / pair) % 64 == 0);
+  if (p.b3d) {
+    const int nch = (tile_t / pair + 63) / 64;
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(T / 64)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(2 * ldb), 128};
+    cuuint32_t box[3] = {64, 128, static_cast<cuuint32_t>(nch)};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(B), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      p.b3d = 0;  // driver refused the chunk-stride map: 2-D boxes below
+  }
+  if (!p.b3d && !encode_b(&tb, contiguous ? 128 : 1)) return VENOM_ERR_CUDA;
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
   if (meta_tc == nullptr) return run_gather<false>(NBg, pair, tile_t, bf16, tv, tb, tv, p, max_ctas, s);
-  // pre-ordered metadata: 2-D [tiles·num_ks·128 rows][4] u32, box 4 × 128 (one 2 KB stage block)
+  // pre-ordered metadata: the [tiles·num_ks] contiguous 2 KB stage blocks, mapped as 2-D
+  // [blocks][256] u64 with a one-row box, so each block is one 2 KB TMA row (a 16-byte-wide box of
+  // 128 rows would cost the TMA unit 128 row requests per stage)
   if (!aligned(meta_tc, 16)) return VENOM_ERR_INVALID_ARGUMENT;
   CUtensorMap te;
   {
-    const int64_t rows = ((R + 127) / 128) * p.num_ks * 128;
-    cuuint64_t dims[2] = {4, static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {16};
-    cuuint32_t box[2] = {4, 128};
+    const int64_t blocks = ((R + 127) / 128) * p.num_ks;
+    cuuint64_t dims[2] = {256, static_cast<cuuint64_t>(blocks)};
+    cuuint64_t strides[1] = {2048};
+    cuuint32_t box[2] = {256, 1};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(meta_tc), dims, strides, box, es,
+    if (enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(meta_tc), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return VENOM_ERR_CUDA;

@@ -3,7 +3,7 @@
 // for CTAs 0/1, then prints per-k-stage event times (ns, relative to the first event).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DVENOM_TRACE \
 //          -o tools/trace_kernels tools/trace_kernels.cu
-// Run:   tools/trace_kernels R K T V M strategy tile_t
+// Run:   tools/trace_kernels R K T V M strategy tile_t pair pre(1: pre-ordered metadata)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -33,7 +33,14 @@ int main(int argc, char** argv) {
   const size_t ntr = 2 * 16 * 256;
   cudaMalloc(&tr, ntr * 8);
   cudaMemcpyToSymbol(g_venom_trace, &tr, sizeof(tr));
-  venom_spmm_opts_t o{tile, 0, 0, strat, pair};
+  const int pre = argc > 9 ? atoi(argv[9]) : 0;
+  uint8_t* mtc = nullptr;
+  if (pre) {
+    const int64_t nb = venom_metadata_tc_bytes(R, K, venom_format_t{V, 2, M});
+    cudaMalloc(&mtc, nb);
+    cudaMemset(mtc, 0x44, nb);
+  }
+  venom_spmm_opts_t o{tile, 0, 0, strat, pair, mtc};
   venom_format_t f{V, 2, M};
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemset(tr, 0, ntr * 8);
