@@ -217,6 +217,7 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
         }
       }
       if (lane == 0) {
+        VENOM_TRACE_EVENT(8, it);
         if constexpr (CG == 2) {
           tc_commit_2sm_mc(empty0 + 8 * stage, 0x3);
           if (ks == p.num_ks - 1) tc_commit_2sm_mc(accf0 + 8 * ab, 0x3);
@@ -256,6 +257,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     const int ab = tl % Cfg::ACC_BUFS;
     mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
     tc_fence_after();
+    if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row = static_cast<int64_t>(m_tile) * (128 * CG) + r_local;
     const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
     const float bv = (p.bias != nullptr && row < p.R)
@@ -314,6 +316,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
         }
         __syncwarp();
       }
+      if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(10, tl);
     } else if (row < p.R) {
       uint16_t* dst = p.C + row * p.ldc + col_base;
 #pragma unroll
@@ -406,7 +409,84 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
   }
 }
 
-template <class Cfg, bool kBF16>
+// M = 4 producer (the 2:4 operand and the #18 re-encoding): B' is a plain K-slice of B, so a stage
+// is three TMA ops. Lane 0 of warp 0 issues expect_tx, the A box(es) and the metadata block(s);
+// lane 0 of warp 1 the B' box (one 3-D box, or one 2-D box per 64-column chunk on warps 1..NCH).
+// Tile coordinates advance incrementally: the whole per-stage cost is a barrier wait and a few
+// instructions (the generic per-stage coordinate computation took longer than the stage's MMAs).
+template <class Cfg>
+__device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const CUtensorMap* tm_values,
+                                                    const CUtensorMap* tm_b, const CUtensorMap* tm_e,
+                                                    int my_tiles, uint32_t smem0, uint32_t full0,
+                                                    uint32_t empty0, uint32_t rank, int warp) {
+  using namespace ptx;
+  constexpr int STAGES = Cfg::STAGES, CG = Cfg::CG, MB = Cfg::MB;
+  const bool b3d = p.b3d != 0;
+  const int role = warp == 0 ? 0 : ((b3d ? warp == 1 : warp <= Cfg::NCH) ? 1 : -1);
+  if (role < 0 || my_tiles == 0) return;
+  const uint64_t pol_a = policy_evict_first();
+  const uint64_t pol_b = policy_evict_last();
+  // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load, 2048 no metadata load
+  const bool do_a = !(p.dbg & 16), do_b = !(p.dbg & 1), do_e = Cfg::PRE && !(p.dbg & 2048);
+  const uint32_t tx = CG * ((do_a ? Cfg::A_BYTES : 0) + (do_b ? Cfg::B_BYTES : 0) + (do_e ? Cfg::E_BYTES : 0));
+  const uint32_t fbar0 = (CG == 2) ? mapa_shared(full0, 0) : full0;
+  const int row_off = 128 * static_cast<int>(rank);
+  int m_tile, n_tile, arow = 0, col0 = 0, eblk0 = 0;
+  auto set_tile = [&](int tl) {
+    tile_coords<CG>(p, tl, m_tile, n_tile);
+    arow = m_tile * 128 * CG * MB + row_off;
+    col0 = n_tile * Cfg::BN + static_cast<int>(rank) * Cfg::BNH;
+    eblk0 = (m_tile * MB * CG + static_cast<int>(rank)) * p.num_ks;
+  };
+  set_tile(0);
+  int tl = 0, ks = 0, stage = 0;
+  uint32_t phase = 0;
+  const int total = my_tiles * p.num_ks;
+  for (int it = 0; it < total; ++it) {
+    mbar_wait(empty0 + 8 * stage, phase ^ 1);
+    const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
+    const uint32_t fbar = fbar0 + 8 * stage;
+    if (role == 0) {
+      VENOM_TRACE_EVENT(0, it);
+      if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
+      if (do_a)
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          if constexpr (CG == 2) tma_load_2d_2sm(sbase + mb * Cfg::A_BLOCK, tm_values, fbar, ks * 64, arow + mb * 128 * CG, pol_a);
+          else tma_load_2d(sbase + mb * Cfg::A_BLOCK, tm_values, fbar, ks * 64, arow + mb * 128 * CG, pol_a);
+        }
+      if (do_e)
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          const uint32_t edst = sbase + Cfg::A_BYTES + Cfg::B_BYTES + mb * Cfg::E_BLOCK;
+          const int eblk = eblk0 + mb * CG * p.num_ks + ks;
+          if constexpr (CG == 2) tma_load_2d_2sm(edst, tm_e, fbar, 0, eblk, pol_a);
+          else tma_load_2d(edst, tm_e, fbar, 0, eblk, pol_a);
+        }
+      VENOM_TRACE_EVENT(4, it);
+    } else if (do_b) {
+      if (b3d) {
+        if constexpr (CG == 2) tma_load_3d_2sm(sbase + Cfg::A_BYTES, tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
+        else tma_load_3d(sbase + Cfg::A_BYTES, tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
+      } else {
+        const int c = warp - 1;
+        if constexpr (CG == 2) tma_load_2d_2sm(sbase + Cfg::A_BYTES + c * Cfg::B_CHUNK, tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
+        else tma_load_2d(sbase + Cfg::A_BYTES + c * Cfg::B_CHUNK, tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
+      }
+      VENOM_TRACE_EVENT(7, it);
+    }
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (++ks == p.num_ks) {
+      ks = 0;
+      if (++tl < my_tiles) set_tile(tl);
+    }
+  }
+}
+
+template <class Cfg, bool kBF16, bool kContig>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
@@ -429,6 +509,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;  // position in the CTA pair
+  if (threadIdx.x == 0) VENOM_TRACE_EVENT(11, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -454,6 +535,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  if (threadIdx.x == 0) VENOM_TRACE_EVENT(11, 1);
 
   const int my_tiles = my_tile_count<CG>(p);
   const int total = my_tiles * p.num_ks;  // k-stage iterations this CTA runs
@@ -467,7 +549,10 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     return rb < nrb ? rb : nrb - 1;  // padding block of a ragged last tile: any valid block
   };
 
-  if (warp < Cfg::P) {
+  if (warp < Cfg::P && kContig) {
+    if (lane == 0)
+      producer_contiguous<Cfg>(p, &tm_values, &tm_b, &tm_e, my_tiles, smem0, full0, empty0, rank, warp);
+  } else if (warp < Cfg::P) {
     // ======================= producers: values tile + gathered B' rows =======================
     // Stage ops are (block b, chunk c, group q); warp w issues ops [w·OPS_PER_WARP, ...), one per
     // lane: TMA issue is serial within a warp, so the gathers are spread over P warps. With a CTA
@@ -652,6 +737,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
+  if (threadIdx.x == 0) VENOM_TRACE_EVENT(11, 2);
   if (warp == Cfg::W_MMA) {
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_2sm<512>(tmem_base);

@@ -105,7 +105,7 @@ venom_status_t launch_cg(Kern kern, int cg, int grid, int threads, int smem, cud
 template <class Cfg, bool kBF16>
 venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUtensorMap& te,
                         SpmmParams p, int max_ctas, cudaStream_t s) {
-  auto kern = venom::vnm_spmm_kernel<Cfg, kBF16>;
+  auto kern = p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true> : venom::vnm_spmm_kernel<Cfg, kBF16, false>;
   // >= 116 KB of shared memory guarantees one CTA per SM (each CTA allocates all 512 TMEM columns)
   const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

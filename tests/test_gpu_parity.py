@@ -247,6 +247,8 @@ SPMM_CASES = [
     (256, 896, 128, 256, 28, BF16, False, 0),  # V = 256 (two 128-row slices share column_idx)
     (256, 1600, 264, 128, 100, F16, True, 0),  # 2:100, K' tail (G = 16)
     (512, 1024, 512, 128, 4, F16, True, 256),  # plain 2:4, tile 256
+    (768, 1024, 512, 128, 4, F16, True, 256),  # 2:4, multicast pair clusters with an idle pair
+    (384, 512, 264, 64, 4, BF16, False, 256),  # 2:4, half-filled cluster tile, T tail
     (512, 1024, 384, 128, 16, F16, True, 192),
     (512, 2048, 256, 128, 32, BF16, False, 64),
     (256, 1024, 256, 64, 8, F16, True, 128),   # V=64 tile 128 (single accumulator)

@@ -3,7 +3,7 @@
 // for CTAs 0/1, then prints per-k-stage event times (ns, relative to the first event).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DVENOM_TRACE \
 //          -o tools/trace_kernels tools/trace_kernels.cu
-// Run:   tools/trace_kernels R K T V M strategy tile_t pair pre(1: pre-ordered metadata)
+// Run:   tools/trace_kernels R K T V M strategy tile_t pair pre(1: pre-ordered metadata) max_ctas
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -40,7 +40,8 @@ int main(int argc, char** argv) {
     cudaMalloc(&mtc, nb);
     cudaMemset(mtc, 0x44, nb);
   }
-  venom_spmm_opts_t o{tile, 0, 0, strat, pair, mtc};
+  const int max_ctas = argc > 10 ? atoi(argv[10]) : 0;
+  venom_spmm_opts_t o{tile, 0, max_ctas, strat, pair, mtc};
   venom_format_t f{V, 2, M};
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemset(tr, 0, ntr * 8);
@@ -61,18 +62,22 @@ int main(int argc, char** argv) {
   for (int k = 0; k < 16; ++k)
     for (int i = 0; i < 256; ++i)
       if (h[k * 256 + i] && h[k * 256 + i] < t0) t0 = h[k * 256 + i];
-  const char* names[8] = {"prodB", "mmaFull", "mmaCommit", "meta/expRaw", "prodDone/expEmpty",
-                          "expArrive", "", ""};
+  const char* names[12] = {"prodB", "mmaFull", "mmaCommit", "meta", "prodDone", "prodTop",
+                           "prodA+", "prodB3d+", "mmaIssued", "epiAcc(tile)", "epiStored(tile)",
+                           "kern(0start,1init,2end)"};
   for (int cta = 0; cta < 2; ++cta) {
     printf("CTA %d\nit ", cta);
-    for (int k = 0; k < 6; ++k) printf("%18s", names[k]);
+    for (int k = 0; k < 12; ++k) printf("%11.11s", names[k]);
     printf("   (ns since first event)\n");
-    for (int i = 0; i < 80; ++i) {
+    for (int i = 0; i < 96; ++i) {
+      bool any = false;
+      for (int k = 0; k < 12; ++k) any |= h[(cta * 16 + k) * 256 + i] != 0;
+      if (!any) continue;
       printf("%3d", i);
-      for (int k = 0; k < 6; ++k) {
+      for (int k = 0; k < 12; ++k) {
         const unsigned long long v = h[(cta * 16 + k) * 256 + i];
-        if (v) printf("%18llu", v - t0);
-        else printf("%18s", "-");
+        if (v) printf("%11lld", (long long)(v - t0));
+        else printf("%11s", "-");
       }
       printf("\n");
     }
