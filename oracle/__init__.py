@@ -30,6 +30,7 @@ UNSUPPORTED_PATTERN = 4
 UNSUPPORTED_DTYPE = 5
 NON_FINITE = 6
 CORRUPT_METADATA = 7
+INVALID_MASK = 10
 
 F16, BF16 = 0, 1
 
@@ -65,6 +66,8 @@ def _load():
         lib.oracle_gemm_dense.argtypes = [P, I64, I64, I64, I, P, I64, I64, P, P, I64]
         lib.oracle_num_threads.argtypes = []
         lib.oracle_expand_2to4.argtypes = [P, P, P, I64, I64, I, I, I, P, P, P]
+        lib.oracle_compress_masked.argtypes = [P, I64, I64, I64, I, P, I64, I, I, I, P, P, P]
+        lib.oracle_energy.argtypes = [P, I64, I64, I64, I, P, I64, P]
         _lib = lib
     return _lib
 
@@ -109,6 +112,41 @@ def compress(A: np.ndarray, dtype: int, V: int, M: int, N: int = 2, check: bool 
             raise OracleError(st, "compress")
         return st
     return values, metadata, cidx
+
+
+def compress_masked(A: np.ndarray, mask: np.ndarray, dtype: int, V: int, M: int, N: int = 2,
+                    check: bool = True):
+    """Compression with the kept set given by an external V:N:M mask (uint8, non-zero = keep);
+    see oracle_compress_masked. Same outputs as compress()."""
+    A = np.asarray(A)
+    mask = np.asarray(mask)
+    assert A.dtype == np.uint16 and A.ndim == 2 and A.strides[1] == 2
+    assert mask.dtype == np.uint8 and mask.shape == A.shape and mask.strides[1] == 1
+    R, K = A.shape
+    G = K // M if M > 0 else 0
+    values = np.zeros((R, max(G, 0), 2), np.uint16)
+    metadata = np.zeros((R, (max(G, 0) + 1) // 2), np.uint8)
+    cidx = np.zeros((R // V if V > 0 else 0, max(G, 0), 4), np.uint8)
+    st = _load().oracle_compress_masked(_ptr(A), R, K, A.strides[0] // 2, dtype, _ptr(mask),
+                                        mask.strides[0], V, N, M, _ptr(values), _ptr(metadata), _ptr(cidx))
+    if st != OK:
+        if check:
+            raise OracleError(st, "compress_masked")
+        return st
+    return values, metadata, cidx
+
+
+def energy(A: np.ndarray, values: np.ndarray, dtype: int):
+    """(kept sum, dense sum, energy) in fp64 — PAPER.md:305-309; see oracle_energy."""
+    A = np.asarray(A)
+    assert A.dtype == np.uint16 and A.ndim == 2 and A.strides[1] == 2
+    v = np.ascontiguousarray(values).reshape(-1)
+    out = np.zeros(3, np.float64)
+    st = _load().oracle_energy(_ptr(A), A.shape[0], A.shape[1], A.strides[0] // 2, dtype, _ptr(v),
+                               v.size, _ptr(out))
+    if st != OK:
+        raise OracleError(st, "energy")
+    return float(out[0]), float(out[1]), float(out[2])
 
 
 def decompress(values, metadata, column_idx, R: int, K: int, dtype: int, V: int, M: int,

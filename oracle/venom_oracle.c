@@ -32,7 +32,8 @@ enum {
   ORC_UNSUPPORTED_PATTERN = 4,
   ORC_UNSUPPORTED_DTYPE = 5,
   ORC_NON_FINITE = 6,
-  ORC_CORRUPT_METADATA = 7
+  ORC_CORRUPT_METADATA = 7,
+  ORC_INVALID_MASK = 10
 };
 
 /* dtype: 0 = IEEE binary16 (fp16, "half precision"), 1 = bfloat16. */
@@ -156,6 +157,99 @@ int oracle_compress(const uint16_t* A, int64_t R, int64_t K, int64_t lda, int dt
   }
   free(s);
   free(taken);
+  return ORC_OK;
+}
+
+/*
+ * Masked compression (reading #20). The kept entries come from an
+ * external mask (mask[i*ldm + k] != 0 keeps A[i][k]), e.g. one chosen by the paper's second-order
+ * pruner, instead of the magnitude rule of PAPER.md:188. The mask must itself be
+ * V:N:M: per V x M block at most 4 distinct columns hold kept entries ("4 columns
+ * ... are selected"), and per row at most N = 2 kept entries per group.
+ *   1. S = the block's columns with a kept entry in any of its V rows, in ascending order; if
+ *      |S| < 4 it is completed with the lowest-index columns not in S (reading #6's fill rule) and
+ *      the four are stored ascending as column_idx.
+ *   2. Per row, P = the m-indices t with mask[i][g*M + c_t] != 0, ascending; if |P| < 2 it is
+ *      completed with the lowest free m-indices. Kept entries store A's raw bits, filled ones +0.0
+ *      (bits 0x0000): the operand is exactly A∘mask.
+ * Returns ORC_INVALID_MASK if some block has |S| > 4 or some row-group |P| > 2.
+ */
+int oracle_compress_masked(const uint16_t* A, int64_t R, int64_t K, int64_t lda, int dtype,
+                           const uint8_t* mask, int64_t ldm, int V, int N, int M,
+                           uint16_t* values, uint8_t* metadata, uint8_t* column_idx) {
+  int st = oracle_validate(R, K, V, N, M);
+  if (st != ORC_OK) return st;
+  if (dtype != 0 && dtype != 1) return ORC_UNSUPPORTED_DTYPE;
+  if (lda < K || ldm < K) return ORC_INVALID_ARGUMENT;
+  for (int64_t i = 0; i < R; ++i)
+    for (int64_t k = 0; k < K; ++k)
+      if (!isfinite(oracle_decode(A[i * lda + k], dtype))) return ORC_NON_FINITE;
+  const int64_t G = K / M;
+  const int64_t meta_row = (G + 1) / 2;
+  memset(metadata, 0, (size_t)(R * meta_row));
+  int* used = (int*)malloc(sizeof(int) * (size_t)M);
+  if (!used) return ORC_INVALID_ARGUMENT;
+  for (int64_t rb = 0; rb < R / V; ++rb) {
+    for (int64_t g = 0; g < G; ++g) {
+      /* step 1: columns of the block that hold a kept entry */
+      int ns = 0;
+      for (int j = 0; j < M; ++j) {
+        used[j] = 0;
+        for (int64_t i = rb * V; i < rb * V + V; ++i)
+          if (mask[i * ldm + g * M + j]) used[j] = 1;
+        ns += used[j];
+      }
+      if (ns > 4) { free(used); return ORC_INVALID_MASK; }
+      for (int j = 0; j < M && ns < 4; ++j)
+        if (!used[j]) { used[j] = 2; ++ns; }          /* fill: lowest free columns */
+      int c[4], n = 0;
+      for (int j = 0; j < M; ++j)
+        if (used[j]) c[n++] = j;                       /* ascending by construction */
+      for (int t = 0; t < 4; ++t) column_idx[(rb * G + g) * 4 + t] = (uint8_t)c[t];
+      /* step 2: per row, the kept m-indices, completed to two */
+      for (int64_t i = rb * V; i < rb * V + V; ++i) {
+        int keep[4], np = 0;
+        for (int t = 0; t < 4; ++t) {
+          keep[t] = mask[i * ldm + g * M + c[t]] != 0;
+          np += keep[t];
+        }
+        if (np > 2) { free(used); return ORC_INVALID_MASK; }
+        int p[2], q = 0;
+        /* the kept positions and the lowest free ones, merged in ascending order */
+        int pick[4] = {0, 0, 0, 0};
+        for (int t = 0; t < 4; ++t) pick[t] = keep[t];
+        for (int t = 0; t < 4 && np < 2; ++t)
+          if (!pick[t]) { pick[t] = 2; ++np; }
+        for (int t = 0; t < 4; ++t)
+          if (pick[t]) p[q++] = t;
+        for (int s2 = 0; s2 < 2; ++s2)
+          values[(i * G + g) * 2 + s2] = (pick[p[s2]] == 1) ? A[i * lda + g * M + c[p[s2]]] : (uint16_t)0x0000;
+        uint8_t nib = (uint8_t)(p[0] | (p[1] << 2));
+        metadata[i * meta_row + g / 2] |= (uint8_t)(nib << (4 * (g % 2)));
+      }
+    }
+  }
+  free(used);
+  return ORC_OK;
+}
+
+/*
+ * Energy of a pruned matrix: the kept magnitude over the dense magnitude,
+ * energy = sum_kept |w_i| / sum_all |w*_i|, both summed in fp64 in ascending index order. The kept
+ * entries are the stored values (n_values of them; filled +0.0 entries add nothing). out[0] = kept
+ * sum, out[1] = dense sum, out[2] = energy, defined as 1 when the dense sum is 0 (reading #21).
+ */
+int oracle_energy(const uint16_t* A, int64_t R, int64_t K, int64_t lda, int dtype,
+                  const uint16_t* values, int64_t n_values, double* out) {
+  if (dtype != 0 && dtype != 1) return ORC_UNSUPPORTED_DTYPE;
+  if (lda < K) return ORC_INVALID_ARGUMENT;
+  double kept = 0.0, all = 0.0;
+  for (int64_t v = 0; v < n_values; ++v) kept += fabs(oracle_decode(values[v], dtype));
+  for (int64_t i = 0; i < R; ++i)
+    for (int64_t k = 0; k < K; ++k) all += fabs(oracle_decode(A[i * lda + k], dtype));
+  out[0] = kept;
+  out[1] = all;
+  out[2] = (all == 0.0) ? 1.0 : kept / all;
   return ORC_OK;
 }
 

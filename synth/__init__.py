@@ -103,3 +103,25 @@ def gaussian_device(shape, std: float, dtype: int, seed: int, device):
     tdt = torch.float16 if dtype == F16 else torch.bfloat16
     x = torch.randn(shape, generator=g, device=device, dtype=torch.float32)
     return (x * std).to(tdt)
+
+
+def vnm_mask(R: int, K: int, V: int, M: int, seed: int, max_cols: int = 4, max_keep: int = 2,
+             p_keep: float = 0.8) -> np.ndarray:
+    """A random keep-mask with V:N:M structure (uint8, 1 = keep): per V x M block a random set of
+    at most `max_cols` columns, per row and group at most `max_keep` of them, each candidate kept
+    with probability `p_keep` (so some blocks / rows use fewer — the fill cases). Stands in for an
+    external pruner's output (e.g. second-order); no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    mask = np.zeros((R, K), np.uint8)
+    for rb in range(R // V):
+        for g in range(K // M):
+            ncols = int(rng.integers(0, max_cols + 1))
+            cols = rng.choice(M, size=ncols, replace=False)
+            for i in range(rb * V, rb * V + V):
+                if ncols == 0:
+                    continue
+                k = int(rng.integers(0, min(max_keep, ncols) + 1))
+                for c in rng.choice(cols, size=k, replace=False):
+                    if rng.random() < p_keep:
+                        mask[i, g * M + int(c)] = 1
+    return mask

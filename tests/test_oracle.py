@@ -345,3 +345,87 @@ def test_expand_2to4_m4_identity_and_rules():
     # subgroup 0 (cols 0-3): a at position 1 -> (0, a) at (0, 1); subgroup 1 (cols 4-7): b at 2 -> (0, b) at (0, 2)
     assert v2.tolist() == [[[0, int(a)], [0, int(b)]]]
     assert m2.tolist() == [[(0 | 1 << 2) | ((0 | 2 << 2) << 4)]]
+
+
+# --------------------------------------------------------------------------- masked compression
+# SURVEY §8(f) rank 4 / DESIGN.md readings #20-#21: the kept set from an external V:N:M mask.
+@pytest.mark.parametrize("name", ["P7_masked_compress.json", "P8_masked_fill.json"])
+def test_compress_masked_golden(name):
+    g = load_golden(name)
+    A, dt = _golden_bits(g, "A", "A_bits")
+    mask = np.array(g["mask"], np.uint8)
+    values, meta, cidx = oracle.compress_masked(A, mask, dt, V=g["V"], M=g["M"], N=g["N"])
+    assert cidx.tolist() == g["expected_column_idx"]
+    assert meta.tolist() == g["expected_metadata"]
+    exp_vals, _ = _golden_bits(g, "expected_values", "expected_values_bits")
+    assert np.array_equal(values, exp_vals)
+    assert oracle.energy(A, values, dt)[2] == pytest.approx(g["expected_energy"], rel=1e-15)
+
+
+@pytest.mark.parametrize("R,K,V,M,dt,seed", [(8, 64, 4, 8, F16, 1), (16, 96, 8, 16, BF16, 2),
+                                             (12, 40, 3, 10, F16, 3), (4, 32, 1, 4, F16, 4)])
+def test_compress_masked_roundtrip_is_A_times_mask(R, K, V, M, dt, seed):
+    """decompress(compress_masked(A, m)) == A∘m bit for bit, with pruned entries +0.0 (the operand
+    is exactly the masked matrix); A∘m written with numpy, not the oracle."""
+    A = synth.gaussian((R, K), 1.0, dt, seed)
+    m = synth.vnm_mask(R, K, V, M, seed + 100)
+    v, md, c = oracle.compress_masked(A, m, dt, V=V, M=M)
+    D = oracle.decompress(v, md, c, R, K, dt, V, M)
+    assert np.array_equal(D, np.where(m != 0, A, np.uint16(0)))
+    # every kept entry is addressed by the metadata; every stored position is kept or +0.0
+    kept = mask_from_compressed(md, c, R, K, V, M)
+    assert not (m.astype(bool) & ~kept).any()
+    # the shape identities of PAPER.md:194-195 and the ascending invariants (SPEC.md:52-53)
+    assert v.size == R * (K // M) * 2 and c.size == (R // V) * (K // M) * 4
+    assert (np.diff(c.astype(int), axis=2) > 0).all()
+
+
+def test_compress_masked_with_the_magnitude_mask_equals_compress():
+    """Independent formulation: feeding the magnitude compressor's own kept set as
+    the external mask reproduces the same matrix (decompressed bit for bit)."""
+    R, K, V, M = 16, 128, 8, 8
+    A = synth.gaussian((R, K), 1.0, F16, 9)
+    v, md, c = oracle.compress(A, F16, V=V, M=M)
+    m = mask_from_compressed(md, c, R, K, V, M).astype(np.uint8)
+    v2, md2, c2 = oracle.compress_masked(A, m, F16, V=V, M=M)
+    assert np.array_equal(oracle.decompress(v2, md2, c2, R, K, F16, V, M),
+                          oracle.decompress(v, md, c, R, K, F16, V, M))
+
+
+def test_compress_masked_rejects_non_vnm_masks():
+    """A mask with 5 columns in one V x M block, or 3 kept entries in one row-group, is not V:N:M
+    (PAPER.md:187-189): status INVALID_MASK."""
+    A = synth.gaussian((4, 16), 1.0, F16, 5)
+    m = np.zeros((4, 16), np.uint8)
+    m[0, [0, 1]] = 1
+    m[1, [2, 3]] = 1
+    m[2, [4]] = 1  # fifth column of block (rows 0-3, cols 0-7)
+    assert oracle.compress_masked(A, m, F16, V=4, M=8, check=False) == oracle.INVALID_MASK
+    m[:] = 0
+    m[3, [8, 9, 10]] = 1  # three kept in one row-group
+    assert oracle.compress_masked(A, m, F16, V=4, M=8, check=False) == oracle.INVALID_MASK
+    m[:] = 0
+    m[3, [8, 9]] = 1
+    assert isinstance(oracle.compress_masked(A, m, F16, V=4, M=8, check=False), tuple)
+
+
+def test_energy_definition_and_special_cases():
+    """energy = sum|kept| / sum|dense|, against numpy on A∘mask; 1 when nothing
+    is pruned (an already V:N:M matrix), 1 for an all-zero matrix (reading #21), and within (0, 1]."""
+    R, K, V, M = 8, 64, 4, 8
+    A = synth.gaussian((R, K), 1.0, F16, 11)
+    v, md, c = oracle.compress(A, F16, V=V, M=M)
+    kept, dense, e = oracle.energy(A, v, F16)
+    m = mask_from_compressed(md, c, R, K, V, M)
+    a = np.abs(bits_to_f64(A, F16))
+    assert dense == pytest.approx(a.sum(), rel=1e-14)
+    assert kept == pytest.approx(a[m].sum(), rel=1e-14)
+    assert 0.0 < e <= 1.0 and e == pytest.approx(a[m].sum() / a.sum(), rel=1e-14)
+    D = oracle.decompress(v, md, c, R, K, F16, V, M)        # already V:N:M: nothing left to prune
+    v2, _, _ = oracle.compress(D, F16, V=V, M=M)
+    assert oracle.energy(D, v2, F16)[2] == pytest.approx(1.0, rel=1e-15)
+    Z = np.zeros((R, K), np.uint16)
+    vz, _, _ = oracle.compress(Z, F16, V=V, M=M)
+    assert oracle.energy(Z, vz, F16) == (0.0, 0.0, 1.0)
+    # magnitude pruning keeps at least the 2/M fraction of the mass that a uniform keep would
+    assert e >= 2.0 / M
