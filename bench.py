@@ -50,9 +50,10 @@ for _k in synth.WORKLOADS:
 DEFAULT_WORKLOAD = "bert_large_ffn_4096tok_64:2:8"
 
 
-# measured TMA L2 -> SMEM landing ceiling per SM (GB/s): tools/microbench_stream.cu,
-# profiles/r01_microbench_stream.txt (64.8-65.2 B/ns per SM with multicast, 49 without)
-FEED_CEILING_GBPS_PER_SM = 65.0
+# measured TMA L2 -> SMEM landing ceiling per SM (GB/s): the SpMM's own steady-state stage rate
+# with the L2 idle (8 CTAs: 50 KB per 590 ns per SM, the same as with 148 CTAs, so a per-SM limit;
+# profiles/r01_trace_spmm_bert_ffn2_grid8.txt). Higher than tools/microbench_stream.cu's 65 B/ns.
+FEED_CEILING_GBPS_PER_SM = 86.8
 
 
 def useful_flops(w) -> float:
@@ -362,12 +363,12 @@ def run_gpu(args, ws, rank, local):
             if xb and len(xb) == len(per_launch_ms):
                 # the on-chip feed that binds these kernels: L2 -> SMEM bytes per
                 # launch (ncu l1tex__m_xbar2l1tex_read_bytes) over the live launch time, against the
-                # measured per-SM landing ceiling × SMs (tools/microbench_stream.cu)
+                # measured per-SM landing ceiling × SMs (FEED_CEILING_GBPS_PER_SM)
                 ach = sum(xb) / (sum(per_launch_ms) / 1e3) / 1e9
                 ceil = FEED_CEILING_GBPS_PER_SM * torch.cuda.get_device_properties(device).multi_processor_count
                 feed = {"l2_to_smem_bytes_per_launch": xb, "achieved_GBps": round(ach, 1),
                         "ceiling_GBps": round(ceil, 1), "frac": round(ach / ceil, 4),
-                        "ceiling_source": "profiles/r01_microbench_stream.txt (TMA landing, multicast)"}
+                        "ceiling_source": "profiles/r01_trace_spmm_bert_ffn2_grid8.txt (SpMM stage rate per SM, L2 idle)"}
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_burst, 4), "traffic": traffic,
                 "peak_source": f"{peak_src} bf16 dense burst (fp16 1:1); useful FLOPs of a 2:4 sparse "
