@@ -52,7 +52,10 @@ typedef enum {
   VENOM_ERR_CORRUPT_METADATA = 7,    /* device-reported: m-indices not ascending, column_idx not
                                         strictly ascending or >= M                  */
   VENOM_ERR_ARCH = 8,                /* current device is not sm_100                             */
-  VENOM_ERR_CUDA = 9                 /* launch / driver error                                    */
+  VENOM_ERR_CUDA = 9,                /* launch / driver error                                    */
+  VENOM_ERR_INVALID_MASK = 10        /* device-reported by venom_compress_masked: the mask is not
+                                        V:N:M (> 4 columns in a V×M block or > 2 kept entries in a
+                                        row of a group)                                         */
 } venom_status_t;
 
 typedef enum { VENOM_F16 = 0, VENOM_BF16 = 1 } venom_dtype_t;
@@ -84,6 +87,34 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda,
                               venom_dtype_t dt, venom_format_t f,
                               void* values, uint8_t* metadata, uint8_t* column_idx,
                               int32_t* dev_status, venom_stream_t stream);
+
+/*
+ * Masked V:N:M compression (reading #20): the kept entries come from
+ * an external mask (e.g. a second-order pruner) instead of the magnitude rule.
+ *   mask   uint8[R][ldm] row-major, ldm >= K; non-zero keeps A[i][k]. It must be V:N:M: at most 4
+ *          columns of each V×M block hold kept entries and at most 2 per row of each group, else
+ *          VENOM_ERR_INVALID_MASK is reported through dev_status (outputs undefined).
+ *   column_idx: the block's kept columns, completed to 4 with the lowest-index free columns,
+ *   ascending; per row the kept m-indices completed to 2 with the lowest free ones; kept entries
+ *   store A's raw bits, filled ones +0.0 — so decompress(result) == A∘mask bit for bit.
+ * Requirements: as venom_compress. Bit-identical to the CPU oracle. Offline (once per weight).
+ */
+venom_status_t venom_compress_masked(const void* A, int64_t R, int64_t K, int64_t lda,
+                                     const uint8_t* mask, int64_t ldm, venom_dtype_t dt,
+                                     venom_format_t f, void* values, uint8_t* metadata,
+                                     uint8_t* column_idx, int32_t* dev_status, venom_stream_t stream);
+
+/*
+ * Energy of a pruned matrix: energy = Σ|kept| / Σ|dense|, both in fp64.
+ *   A        dtype[R][lda], the dense matrix w*
+ *   values   dtype[n_values], the kept values (e.g. a compressed operand's values array; filled
+ *            +0.0 entries add nothing)
+ *   out      DEVICE double[3]: {Σ|kept|, Σ|dense|, energy}; energy = 1 when Σ|dense| = 0.
+ * The sums are fp64 over per-CTA partials (order differs from the oracle's: equal to ≤ 1e-12
+ * relative). Writes `out` on the stream; no host synchronisation.
+ */
+venom_status_t venom_energy(const void* A, int64_t R, int64_t K, int64_t lda, const void* values,
+                            int64_t n_values, venom_dtype_t dt, double* out, venom_stream_t stream);
 
 /*
  * Inverse of the format: A_out[i][g*M + column_idx[i/V][g][p]] = value with

@@ -27,13 +27,13 @@ STATUS_NAMES = {
     0: "VENOM_OK", 1: "VENOM_ERR_INVALID_ARGUMENT", 2: "VENOM_ERR_NON_DIVISIBLE_ROWS",
     3: "VENOM_ERR_NON_DIVISIBLE_COLS", 4: "VENOM_ERR_UNSUPPORTED_PATTERN",
     5: "VENOM_ERR_UNSUPPORTED_DTYPE", 6: "VENOM_ERR_NON_FINITE", 7: "VENOM_ERR_CORRUPT_METADATA",
-    8: "VENOM_ERR_ARCH", 9: "VENOM_ERR_CUDA",
+    8: "VENOM_ERR_ARCH", 9: "VENOM_ERR_CUDA", 10: "VENOM_ERR_INVALID_MASK",
 }
 EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
             "venom_spmm_ex", "venom_expand_2to4", "venom_compress_2to4", "venom_prefer_2to4",
             "venom_metadata_tc_bytes",
             "venom_order_metadata", "venom_kernels_per_call", "venom_status_string",
-            "venom_version"]
+            "venom_version", "venom_compress_masked", "venom_energy"]
 
 
 class VenomError(RuntimeError):
@@ -79,6 +79,8 @@ def lib() -> ctypes.CDLL:
         L.venom_metadata_tc_bytes.restype = I64
         L.venom_order_metadata.argtypes = [P, I64, I64, _Format, P, P]
         L.venom_compress_2to4.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P, P, P]
+        L.venom_compress_masked.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, _Format, P, P, P, P, P]
+        L.venom_energy.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, P, P]
         L.venom_prefer_2to4.restype = ctypes.c_int
         L.venom_spmm_ex.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int,
                                     ctypes.POINTER(_Opts), P]
@@ -175,6 +177,50 @@ def compress(A: torch.Tensor, V: int, M: int, N: int = 2, status: Optional[torch
         s = int(status.item())
         _check(s, "venom_compress (device status)")
     return VNMTensor(values, metadata, column_idx, R, K, V, M, N)
+
+
+def compress_masked(A: torch.Tensor, mask: torch.Tensor, V: int, M: int, N: int = 2,
+                    status: Optional[torch.Tensor] = None, check: bool = False) -> VNMTensor:
+    """V:N:M compression of ``A`` with the kept set given by an external V:N:M ``mask`` (uint8 or
+    bool, non-zero keeps; e.g. from a second-order pruner). The result is exactly
+    A∘mask. ``check=True`` raises on a non-V:N:M mask or non-finite input."""
+    assert A.is_cuda and A.dim() == 2 and A.stride(1) == 1, "A: 2-D CUDA tensor, unit column stride"
+    if mask.dtype == torch.bool:
+        mask = mask.view(torch.uint8)
+    assert mask.dtype == torch.uint8 and mask.shape == A.shape and mask.stride(1) == 1 and mask.device == A.device
+    R, K = A.shape
+    compressed_sizes(R, K, V, M, N)
+    G = K // M
+    values = torch.empty((R, G, 2), dtype=A.dtype, device=A.device)
+    metadata = torch.empty((R, (G + 1) // 2), dtype=torch.uint8, device=A.device)
+    column_idx = torch.empty((R // V, G, 4), dtype=torch.uint8, device=A.device)
+    if check and status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=A.device)
+    st = lib().venom_compress_masked(ctypes.c_void_p(A.data_ptr()), R, K, A.stride(0),
+                                     ctypes.c_void_p(mask.data_ptr()), mask.stride(0), _dt(A.dtype),
+                                     _Format(V, N, M), ctypes.c_void_p(values.data_ptr()),
+                                     ctypes.c_void_p(metadata.data_ptr()), ctypes.c_void_p(column_idx.data_ptr()),
+                                     ctypes.c_void_p(status.data_ptr() if status is not None else 0),
+                                     _stream(A.device))
+    _check(st, "venom_compress_masked")
+    if check:
+        _check(int(status.item()), "venom_compress_masked (device status)")
+    return VNMTensor(values, metadata, column_idx, R, K, V, M, N)
+
+
+def energy(A: torch.Tensor, kept: "VNMTensor | torch.Tensor", out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Energy of a pruning on the GPU: float64[3] {Σ|kept|, Σ|dense|, energy}.
+    ``kept`` is a compressed operand (its values) or any tensor of kept values."""
+    assert A.is_cuda and A.dim() == 2 and A.stride(1) == 1
+    vals = kept.values if isinstance(kept, VNMTensor) else kept
+    assert vals.is_contiguous() and vals.dtype == A.dtype
+    if out is None:
+        out = torch.empty(3, dtype=torch.float64, device=A.device)
+    st = lib().venom_energy(ctypes.c_void_p(A.data_ptr()), A.shape[0], A.shape[1], A.stride(0),
+                            ctypes.c_void_p(vals.data_ptr()), vals.numel(), _dt(A.dtype),
+                            ctypes.c_void_p(out.data_ptr()), _stream(A.device))
+    _check(st, "venom_energy")
+    return out
 
 
 def decompress(x: VNMTensor, out: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None,

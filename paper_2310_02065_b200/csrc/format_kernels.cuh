@@ -676,4 +676,135 @@ __global__ void __launch_bounds__(256) vnm_order_metadata_kernel(const uint8_t* 
   }
 }
 
+// ------------------------------------------------------------------ masked compression
+// venom_compress_masked (include/venom.h; reading #20): the kept set comes from an
+// external V:N:M mask. One thread per (row block, pair of groups) so that every metadata byte has
+// a single writer. Per group: the block's kept columns (a bitmap over M <= 256 columns), completed
+// to four with the lowest free columns; per row the kept m-indices, completed to two with the
+// lowest free ones; raw bits for kept entries, +0.0 for filled ones. Offline (once per weight):
+// exact and simple rather than fast.
+constexpr int kStatusInvalidMask = 10;
+
+template <bool kBF16>
+__global__ void vnm_compress_masked_kernel(const uint16_t* __restrict__ A, const uint8_t* __restrict__ mask,
+                                           int64_t R, int64_t K, int64_t lda, int64_t ldm, int V, int M,
+                                           int64_t G, uint16_t* __restrict__ values,
+                                           uint8_t* __restrict__ metadata, uint8_t* __restrict__ column_idx,
+                                           int32_t* __restrict__ status) {
+  const int64_t H = (G + 1) / 2;  // metadata bytes per row
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= (R / V) * H) return;
+  const int64_t rb = t / H, h = t - rb * H;
+  bool bad = false, invalid = false;
+  for (int64_t i = rb * V; i < rb * V + V; ++i) {
+    const uint16_t* arow = A + i * lda;
+    for (int64_t k = 2 * h * M; k < (2 * h + 2) * M && k < K; ++k) bad |= bits_non_finite<kBF16>(arow[k]);
+  }
+  for (int gg = 0; gg < 2; ++gg) {
+    const int64_t g = 2 * h + gg;
+    if (g >= G) break;
+    // kept columns of the block
+    uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t i = rb * V; i < rb * V + V; ++i) {
+      const uint8_t* mrow = mask + i * ldm + g * M;
+      for (int j = 0; j < M; ++j)
+        if (mrow[j]) used[j >> 5] |= 1u << (j & 31);
+    }
+    int n = 0;
+    for (int w = 0; w < 8; ++w) n += __popc(used[w]);
+    if (n > 4) invalid = true;
+    int c[4] = {0, 1, 2, 3};
+    {
+      int fill = 4 - n, q = 0;
+      for (int j = 0; j < M && q < 4; ++j) {
+        const bool u = (used[j >> 5] >> (j & 31)) & 1u;
+        if (u || fill > 0) {
+          if (!u) --fill;
+          c[q++] = j;
+        }
+      }
+    }
+    const uint32_t word = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) |
+                          (static_cast<uint32_t>(c[2]) << 16) | (static_cast<uint32_t>(c[3]) << 24);
+    reinterpret_cast<uint32_t*>(column_idx)[rb * G + g] = word;
+    for (int64_t i = rb * V; i < rb * V + V; ++i) {
+      const uint8_t* mrow = mask + i * ldm + g * M;
+      int keep[4], np = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        keep[q] = mrow[c[q]] != 0;
+        np += keep[q];
+      }
+      if (np > 2) invalid = true;
+      int p0 = -1, p1 = -1, need = 2 - np;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bool take = keep[q];
+        if (!take && need > 0) {
+          take = true;
+          --need;
+        }
+        if (take) {
+          if (p0 < 0) p0 = q;
+          else if (p1 < 0) p1 = q;
+        }
+      }
+      if (p1 < 0) p1 = (p0 == 3) ? 2 : 3;  // only on invalid masks (outputs undefined)
+      const uint16_t* arow = A + i * lda + g * M;
+      const uint16_t v0 = keep[p0] ? arow[c[p0]] : static_cast<uint16_t>(0);
+      const uint16_t v1 = keep[p1] ? arow[c[p1]] : static_cast<uint16_t>(0);
+      reinterpret_cast<uint32_t*>(values)[i * G + g] = static_cast<uint32_t>(v0) | (static_cast<uint32_t>(v1) << 16);
+      const uint8_t nib = static_cast<uint8_t>(p0 | (p1 << 2));
+      uint8_t* mb = metadata + i * H + h;
+      *mb = (gg == 0) ? nib : static_cast<uint8_t>(*mb | (nib << 4));
+    }
+  }
+  if (status != nullptr) {
+    if (bad) atomicMax(status, kStatusNonFinite);
+    if (invalid) atomicMax(status, kStatusInvalidMask);
+  }
+}
+
+// ------------------------------------------------------------------ energy
+// out[0] += Σ|values|, out[1] += Σ|A| in fp64: rows of A grid-strided over CTAs, columns over
+// threads (coalesced); one warp-shuffle + shared-memory reduction and two atomics per CTA.
+template <bool kBF16>
+__global__ void __launch_bounds__(256) vnm_energy_kernel(const uint16_t* __restrict__ A, int64_t R, int64_t K,
+                                                         int64_t lda, const uint16_t* __restrict__ values,
+                                                         int64_t nv, double* __restrict__ out) {
+  double kept = 0.0, all = 0.0;
+  for (int64_t i = blockIdx.x; i < R; i += gridDim.x) {
+    const uint16_t* row = A + i * lda;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) all += static_cast<double>(fabsf(bits_to_float<kBF16>(row[k])));
+  }
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nv;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    kept += static_cast<double>(fabsf(bits_to_float<kBF16>(values[v])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kept += __shfl_xor_sync(0xFFFFFFFFu, kept, o);
+    all += __shfl_xor_sync(0xFFFFFFFFu, all, o);
+  }
+  __shared__ double sk[8], sa[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sk[w] = kept;
+    sa[w] = all;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double k2 = 0.0, a2 = 0.0;
+    for (int j = 0; j < static_cast<int>(blockDim.x >> 5); ++j) {
+      k2 += sk[j];
+      a2 += sa[j];
+    }
+    atomicAdd(out, k2);
+    atomicAdd(out + 1, a2);
+  }
+}
+
+__global__ void vnm_energy_finish_kernel(double* out) {
+  out[2] = (out[1] == 0.0) ? 1.0 : out[0] / out[1];
+}
+
 }  // namespace venom

@@ -244,6 +244,7 @@ const char* venom_status_string(venom_status_t s) {
     case VENOM_ERR_CORRUPT_METADATA: return "corrupt metadata";
     case VENOM_ERR_ARCH: return "device is not sm_100";
     case VENOM_ERR_CUDA: return "CUDA error";
+    case VENOM_ERR_INVALID_MASK: return "mask is not V:N:M";
   }
   return "unknown status";
 }
@@ -365,6 +366,57 @@ venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t 
       static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gt, static_cast<uint16_t*>(values),
       metadata, column_idx, dev_status, static_cast<uint32_t*>(values_2to4),
       reinterpret_cast<uint32_t*>(metadata_2to4_tc), debug_flags());
+  return launch_status();
+}
+
+venom_status_t venom_compress_masked(const void* A, int64_t R, int64_t K, int64_t lda,
+                                     const uint8_t* mask, int64_t ldm, venom_dtype_t dt,
+                                     venom_format_t f, void* values, uint8_t* metadata,
+                                     uint8_t* column_idx, int32_t* dev_status, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (lda < K || ldm < K) return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!A || !mask || !values || !metadata || !column_idx) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(values, 4) || !aligned(column_idx, 4) || !aligned(A, 2)) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m;
+  const int64_t n = (R / f.v) * ((G + 1) / 2);
+  const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dt == VENOM_BF16)
+    venom::vnm_compress_masked_kernel<true><<<blocks, 128, 0, s>>>(
+        static_cast<const uint16_t*>(A), mask, R, K, lda, ldm, f.v, f.m, G, static_cast<uint16_t*>(values),
+        metadata, column_idx, dev_status);
+  else
+    venom::vnm_compress_masked_kernel<false><<<blocks, 128, 0, s>>>(
+        static_cast<const uint16_t*>(A), mask, R, K, lda, ldm, f.v, f.m, G, static_cast<uint16_t*>(values),
+        metadata, column_idx, dev_status);
+  return launch_status();
+}
+
+venom_status_t venom_energy(const void* A, int64_t R, int64_t K, int64_t lda, const void* values,
+                            int64_t n_values, venom_dtype_t dt, double* out, venom_stream_t stream) {
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (R < 0 || K < 0 || n_values < 0 || lda < K || !out || (R * K > 0 && !A) || (n_values > 0 && !values))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(out, 8) || !aligned(A, 2) || !aligned(values, 2)) return VENOM_ERR_INVALID_ARGUMENT;
+  venom_status_t st = check_arch();
+  if (st != VENOM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(out, 0, 2 * sizeof(double), s) != cudaSuccess) return VENOM_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(sms * 8);
+  if (dt == VENOM_BF16)
+    venom::vnm_energy_kernel<true><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(A), R, K, lda,
+                                                        static_cast<const uint16_t*>(values), n_values, out);
+  else
+    venom::vnm_energy_kernel<false><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(A), R, K, lda,
+                                                         static_cast<const uint16_t*>(values), n_values, out);
+  venom::vnm_energy_finish_kernel<<<1, 1, 0, s>>>(out);
   return launch_status();
 }
 

@@ -122,6 +122,20 @@ def test_compress_argument_errors(L):
     assert L.venom_decompress(f, f, f, 8, 16, 0, venom._Format(4, 2, 3), f, 16, P(0), P(0)) == 4
 
 
+def test_masked_compress_and_energy_argument_errors(L):
+    P = ctypes.c_void_p
+    f = P(0x10000)
+    fmt = venom._Format(4, 2, 8)
+    assert L.venom_compress_masked(f, 10, 16, 16, f, 16, 0, fmt, f, f, f, P(0), P(0)) == 2  # V ∤ R
+    assert L.venom_compress_masked(f, 8, 16, 16, f, 8, 0, fmt, f, f, f, P(0), P(0)) == 1   # ldm < K
+    assert L.venom_compress_masked(f, 8, 16, 16, P(0), 16, 0, fmt, f, f, f, P(0), P(0)) == 1  # no mask
+    assert L.venom_compress_masked(f, 8, 16, 16, f, 16, 3, fmt, f, f, f, P(0), P(0)) == 5
+    assert L.venom_energy(f, 8, 16, 8, f, 4, 0, f, P(0)) == 1      # lda < K
+    assert L.venom_energy(f, 8, 16, 16, f, 4, 0, P(0), P(0)) == 1  # no output
+    assert L.venom_energy(f, 8, 16, 16, f, 4, 9, f, P(0)) == 5
+    assert L.venom_status_string(10) == b"mask is not V:N:M"
+
+
 def test_no_cpu_fallback_without_device(L):
     """On a GPU-less host a valid call must fail loudly (CUDA / arch error), never compute."""
     import torch

@@ -553,3 +553,73 @@ def test_sparse_encoder_matches_dense_on_pruned_weights():
     yd = enc.dense_forward(cfg, d32, x.float())
     rel = float((ys - yd).norm() / yd.norm())
     assert rel <= 1e-2, rel
+
+
+# ------------------------------------------------------------------ masked compression + energy
+# SURVEY §8(f) rank 4 (readings #20-#21): bit-exact against oracle.compress_masked, the
+# SpMM on the masked operand against the oracle, energy within 1e-12 (fp64, summation order).
+MASKED_CASES = [
+    # (R, K, V, M, kind, dt, p_keep)
+    (128, 512, 64, 8, "gauss", F16, 0.8),
+    (256, 1024, 128, 16, "gauss", BF16, 0.5),
+    (96, 280, 3, 7, "int", F16, 1.0),
+    (64, 200, 32, 10, "special", BF16, 0.7),
+    (40, 500, 1, 100, "gauss", F16, 0.9),
+    (16, 768, 8, 256, "gauss", F16, 0.6),
+]
+
+
+@pytest.mark.parametrize("R,K,V,M,kind,dt,p_keep", MASKED_CASES)
+def test_compress_masked_bit_exact_and_energy(R, K, V, M, kind, dt, p_keep):
+    A = make_input(R, K, kind, dt, 900 + R + K + M, M)
+    mask = synth.vnm_mask(R, K, V, M, 950 + R + M, p_keep=p_keep)
+    ref = oracle.compress_masked(A, mask, dt, V=V, M=M)
+    x = venom.compress_masked(to_dev(A, dt), torch.from_numpy(mask).cuda(), V=V, M=M, check=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_bits(x.values), ref[0])
+    assert np.array_equal(x.metadata.cpu().numpy(), ref[1])
+    assert np.array_equal(x.column_idx.cpu().numpy(), ref[2])
+    e = venom.energy(to_dev(A, dt), x).cpu().numpy()
+    e_ref = oracle.energy(A, ref[0], dt)
+    assert e[0] == pytest.approx(e_ref[0], rel=1e-12, abs=1e-300)
+    assert e[1] == pytest.approx(e_ref[1], rel=1e-12, abs=1e-300)
+    assert e[2] == pytest.approx(e_ref[2], rel=1e-12)
+
+
+def test_compress_masked_golden_and_invalid_masks_on_gpu():
+    for name in ("P7_masked_compress.json", "P8_masked_fill.json"):
+        g = load_golden(name)
+        A = f64_to_bits(np.array(g["A"], np.float64), F16)
+        x = venom.compress_masked(to_dev(A, F16), torch.tensor(g["mask"], dtype=torch.uint8).cuda(),
+                                  V=g["V"], M=g["M"], check=True)
+        assert x.column_idx.cpu().numpy().tolist() == g["expected_column_idx"]
+        assert x.metadata.cpu().numpy().tolist() == g["expected_metadata"]
+        assert bits_to_f64(to_bits(x.values), F16).tolist() == g["expected_values"]
+        assert float(venom.energy(to_dev(A, F16), x)[2]) == pytest.approx(g["expected_energy"], rel=1e-15)
+    A = synth.gaussian((4, 16), 1.0, F16, 5)
+    m = np.zeros((4, 16), np.uint8)
+    m[0, [0, 1]] = 1
+    m[1, [2, 3]] = 1
+    m[2, [4]] = 1          # a fifth column in one V x M block
+    with pytest.raises(venom.VenomError) as ei:
+        venom.compress_masked(to_dev(A, F16), torch.from_numpy(m).cuda(), V=4, M=8, check=True)
+    assert ei.value.status == 10
+    m[:] = 0
+    m[3, [8, 9, 10]] = 1   # three kept entries in one row-group
+    with pytest.raises(venom.VenomError) as ei:
+        venom.compress_masked(to_dev(A, F16), torch.from_numpy(m).cuda(), V=4, M=8, check=True)
+    assert ei.value.status == 10
+
+
+def test_spmm_on_masked_operand_matches_oracle():
+    """The masked operand runs through the unchanged SpMM (gathered and pre-ordered paths)."""
+    R, K, T, V, M = 256, 1024, 256, 128, 8
+    A = synth.gaussian((R, K), 0.02, F16, 31)
+    B = synth.gaussian((K, T), 1.0, F16, 32)
+    mask = synth.vnm_mask(R, K, V, M, 33)
+    v, md, c = oracle.compress_masked(A, mask, F16, V=V, M=M)
+    C_ref = oracle.spmm(v, md, c, R, K, F16, V, M, B)
+    x = venom.compress_masked(to_dev(A, F16), torch.from_numpy(mask).cuda(), V=V, M=M, check=True)
+    check_spmm(venom.spmm(x, to_dev(B, F16)), C_ref, F16)
+    venom.order_metadata(x)
+    check_spmm(venom.spmm(x, to_dev(B, F16), strategy=venom.STRATEGY_GATHER), C_ref, F16)
