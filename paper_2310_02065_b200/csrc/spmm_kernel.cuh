@@ -289,7 +289,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
     if (p.dbg & 4) {  // ablation 4: no C stores
-    } else if (stage_smem != 0) {
+    } else if (stage_smem != 0 && !(p.dbg & 16384)) {  // ablation 16384: direct stores below
       // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
       // store instruction writes 8 rows × 64 contiguous bytes (full sectors) instead of 32 rows ×
       // 16 bytes; 16-byte segments XOR-swizzled by row to keep both passes bank-conflict free
@@ -312,7 +312,8 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
           const int64_t orow = row_base + r;
           const int64_t ocol = col_base + 32 * c + 8 * sgm;
-          if (orow < p.R && ocol < p.T) *reinterpret_cast<uint4*>(p.C + orow * p.ldc + ocol) = o;
+          // ablation 8192: the shared-memory transposes without the global stores
+          if (orow < p.R && ocol < p.T && !(p.dbg & 8192)) *reinterpret_cast<uint4*>(p.C + orow * p.ldc + ocol) = o;
         }
         __syncwarp();
       }
@@ -352,6 +353,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
     tile_coords<CG>(p, tl, m_tile, n_tile);
     mbar_wait(accf0, tl & 1);
     tc_fence_after();
+    if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG * 2) + b * (128 * CG) +
                              128 * static_cast<int>(rank) + 32 * q;
     const int64_t row = row_base + lane;
@@ -373,6 +375,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(mapa_shared(acce0, 0));  // pair leader
+    if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(12, tl);
     if (p.dbg & 4) continue;  // ablation 4: no C stores
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HALF;
     // 32-column chunks (64 B per row), 16 rows at a time through the 1 KB slot: every store
@@ -406,6 +409,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
         __syncwarp();
       }
     }
+    if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(10, tl);
   }
 }
 

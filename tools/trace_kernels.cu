@@ -62,19 +62,19 @@ int main(int argc, char** argv) {
   for (int k = 0; k < 16; ++k)
     for (int i = 0; i < 256; ++i)
       if (h[k * 256 + i] && h[k * 256 + i] < t0) t0 = h[k * 256 + i];
-  const char* names[12] = {"prodB", "mmaFull", "mmaCommit", "meta", "prodDone", "prodTop",
+  const char* names[13] = {"prodB", "mmaFull", "mmaCommit", "meta", "prodDone", "prodTop",
                            "prodA+", "prodB3d+", "mmaIssued", "epiAcc(tile)", "epiStored(tile)",
-                           "kern(0start,1init,2end)"};
+                           "kern(0start,1init,2end)", "epiRel(tile)"};
   for (int cta = 0; cta < 2; ++cta) {
     printf("CTA %d\nit ", cta);
-    for (int k = 0; k < 12; ++k) printf("%11.11s", names[k]);
+    for (int k = 0; k < 13; ++k) printf("%11.11s", names[k]);
     printf("   (ns since first event)\n");
     for (int i = 0; i < 96; ++i) {
       bool any = false;
-      for (int k = 0; k < 12; ++k) any |= h[(cta * 16 + k) * 256 + i] != 0;
+      for (int k = 0; k < 13; ++k) any |= h[(cta * 16 + k) * 256 + i] != 0;
       if (!any) continue;
       printf("%3d", i);
-      for (int k = 0; k < 12; ++k) {
+      for (int k = 0; k < 13; ++k) {
         const unsigned long long v = h[(cta * 16 + k) * 256 + i];
         if (v) printf("%11lld", (long long)(v - t0));
         else printf("%11s", "-");
