@@ -138,6 +138,8 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0
  *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
  *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
+ * R == 0 or T == 0: nothing to compute, VENOM_OK with no launch (leading dimensions are not checked).
+ * K == 0: C = bias broadcast (or 0).
  * metadata may be NULL when opts->metadata_tc is given; column_idx may be NULL when M == 4 (it is the
  * identity and never read).
  * Metadata validity is NOT checked here (use venom_decompress with dev_status to validate);

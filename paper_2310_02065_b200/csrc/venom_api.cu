@@ -521,9 +521,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (strategy == VENOM_STRATEGY_DENSE_K && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (strategy < 0 || strategy > 2) return VENOM_ERR_INVALID_ARGUMENT;
   if (!can_gather && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
-  if (T < 0 || ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
+  if (T < 0) return VENOM_ERR_INVALID_ARGUMENT;
+  if (R == 0 || T == 0) return VENOM_OK;  // nothing to compute (leading dimensions are then moot)
+  if (ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
     return VENOM_ERR_INVALID_ARGUMENT;
-  if (R == 0 || T == 0) return VENOM_OK;
   const bool has_tc = opts && opts->metadata_tc;
   // metadata is not read with pre-ordered metadata; column_idx is not read when M = 4 (identity)
   if (!C || (K > 0 && (!values || !B || (!metadata && !has_tc) || (!column_idx && f.m != 4))))

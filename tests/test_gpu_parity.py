@@ -623,3 +623,57 @@ def test_spmm_on_masked_operand_matches_oracle():
     check_spmm(venom.spmm(x, to_dev(B, F16)), C_ref, F16)
     venom.order_metadata(x)
     check_spmm(venom.spmm(x, to_dev(B, F16), strategy=venom.STRATEGY_GATHER), C_ref, F16)
+
+
+# ------------------------------------------------------------------ full size GPT-3, degenerate shapes
+def test_spmm_full_size_gpt3_sampled():
+    """BASELINE configs[3] (GPT-3 FFN 12288×49152×8192 at 128:2:16) at full size in the bench's
+    launch configuration (gathered kernel, tensor-core-ordered metadata). A and B are drawn on the
+    GPU (bench recipe); the compressor is checked bit-exactly on sampled row blocks (compression is
+    independent per V-row block) and the SpMM on those rows × 32 sampled columns against the oracle."""
+    w = synth.WORKLOADS["gpt3_ffn_12288x49152x8192_128:2:16"]
+    R, K, T, V, M = w["R"], w["K"], w["T"], w["V"], w["M"]
+    sa, sb = synth.seeds(w["cfg"])
+    A = synth.gaussian_device((R, K), 0.02, F16, sa, "cuda")
+    B = synth.gaussian_device((K, T), 1.0, F16, sb, "cuda")
+    x = venom.compress(A, V=V, M=M, check=True)
+    y = venom.order_metadata(x)
+    C = venom.spmm(y, B)
+    torch.cuda.synchronize()
+    rng = np.random.Generator(np.random.PCG64(3))
+    cols = np.sort(rng.choice(T, size=32, replace=False))
+    Bs = to_bits(B[:, torch.from_numpy(cols).cuda()])
+    for rb in (0, 37, R // V - 1):
+        rows = slice(rb * V, rb * V + V)
+        Ab = to_bits(A[rows])
+        v, md, c = oracle.compress(Ab, F16, V=V, M=M)
+        assert np.array_equal(to_bits(x.values[rows]), v)
+        assert np.array_equal(x.metadata[rows].cpu().numpy(), md)
+        assert np.array_equal(x.column_idx[rb:rb + 1].cpu().numpy(), c)
+        C_ref = oracle.spmm(v, md, c, V, K, F16, V, M, Bs)
+        check_spmm(C[rows][:, torch.from_numpy(cols).cuda()], C_ref, F16)
+
+
+def test_spmm_degenerate_shapes():
+    """Empty and minimal problems (include/venom.h): T = 8 (the minimum), one V-block, K = 0
+    (C = bias), R = 0 and T = 0 (nothing to do, no error)."""
+    # T = 8, a single 64-row block
+    R, K, T, V, M = 64, 256, 8, 64, 8
+    A = synth.gaussian((R, K), 0.02, F16, 61)
+    B = synth.gaussian((K, T), 1.0, F16, 62)
+    parts = oracle.compress(A, F16, V=V, M=M)
+    C_ref = oracle.spmm(*parts, R, K, F16, V, M, B)
+    x = venom.compress(to_dev(A, F16), V=V, M=M, check=True)
+    check_spmm(venom.spmm(x, to_dev(B, F16)), C_ref, F16)
+    venom.order_metadata(x)
+    check_spmm(venom.spmm(x, to_dev(B, F16)), C_ref, F16)
+    # K = 0: C = bias broadcast (nothing to multiply)
+    bias = to_dev(synth.gaussian((128,), 0.5, F16, 63), F16)
+    x0 = venom.compress(torch.empty((128, 0), dtype=torch.float16, device="cuda"), V=64, M=8)
+    C0 = venom.spmm(x0, torch.empty((0, 16), dtype=torch.float16, device="cuda"), bias=bias)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, bias[:, None].expand(128, 16))
+    # R = 0 and T = 0
+    xr = venom.compress(torch.empty((0, 64), dtype=torch.float16, device="cuda"), V=64, M=8)
+    assert venom.spmm(xr, torch.randn(64, 16, device="cuda").half()).shape == (0, 16)
+    assert venom.spmm(x, torch.empty((K, 0), dtype=torch.float16, device="cuda")).shape == (R, 0)
