@@ -218,6 +218,11 @@ typedef struct {
                         order (venom_order_metadata). When set, the gathered kernel loads it with
                         TMA and copies it to TMEM with tcgen05.cp instead of permuting `metadata`
                         on the fly; `metadata` is then not read. Must be 16-byte aligned. */
+  int32_t c_transposed;  /* 1: C is written token-major, C^T = dtype[T][ldc] with ldc >= R
+                        (element (r, t) at C[t*ldc + r]; ldc % 8 == 0) — the layout attention and
+                        a PyTorch [tokens, features] activation use. Gathered / contiguous kernel
+                        with one 128-row accumulator per CTA only (tile_t 240 and DENSE_K are
+                        rejected with VENOM_ERR_INVALID_ARGUMENT). 0: row-major C (default). */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

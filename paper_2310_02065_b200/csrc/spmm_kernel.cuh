@@ -47,6 +47,7 @@ struct SpmmParams {
   int num_tiles;
   int is_bf16;
   int b3d;  // M = 4: B map is 3-D [T/64][K][64] (one box per stage) instead of 2-D
+  int c_t;  // C stored transposed (token-major): element (r, t) at C[t * ldc + r]
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -288,7 +289,20 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       else mbar_arrive(acce0 + 8 * ab);
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
-    if (p.dbg & 4) {  // ablation 4: no C stores
+    if (p.c_t) {
+      // token-major C (C^T[t][r]): for each column t the warp's 32 lanes hold 32 consecutive rows,
+      // so one 16-bit store per lane writes 64 contiguous bytes of C^T row t — coalesced as is
+      if (row < p.R) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int64_t t = col_base + 32 * c + j;
+            if (32 * c + j < HC && t < p.T)
+              p.C[t * p.ldc + row] = static_cast<uint16_t>((pk[c][j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+          }
+      }
+    } else if (p.dbg & 4) {  // ablation 4: no C stores
     } else if (stage_smem != 0 && !(p.dbg & 16384)) {  // ablation 16384: direct stores below
       // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
       // store instruction writes 8 rows × 64 contiguous bytes (full sectors) instead of 32 rows ×
@@ -749,14 +763,13 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   }
 }
 
-// C = bias (or 0) when K == 0 (no groups): nothing to multiply.
-template <bool kBF16>
-__global__ void vnm_fill_bias_kernel(uint16_t* C, int64_t R, int64_t T, int64_t ldc,
-                                     const uint16_t* bias) {
+// C = bias (or 0) when K == 0 (no groups): nothing to multiply. transposed: C^T[t][r] layout.
+__global__ void vnm_fill_bias_kernel(uint16_t* C, int64_t R, int64_t T, int64_t ldc, const uint16_t* bias,
+                                     int transposed) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= R * T) return;
   const int64_t r = idx / T, t = idx - r * T;
-  C[r * ldc + t] = bias ? bias[r] : static_cast<uint16_t>(0);
+  C[transposed ? t * ldc + r : r * ldc + t] = bias ? bias[r] : static_cast<uint16_t>(0);
 }
 
 }  // namespace venom

@@ -521,9 +521,12 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (strategy == VENOM_STRATEGY_DENSE_K && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (strategy < 0 || strategy > 2) return VENOM_ERR_INVALID_ARGUMENT;
   if (!can_gather && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
+  const bool ct = opts && opts->c_transposed;  // token-major C^T[T][ldc]
   if (T < 0) return VENOM_ERR_INVALID_ARGUMENT;
   if (R == 0 || T == 0) return VENOM_OK;  // nothing to compute (leading dimensions are then moot)
-  if (ldb < T || ldc < T || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
+  if (ldb < T || (ct ? ldc < R : ldc < T) || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (ct && (strategy == VENOM_STRATEGY_DENSE_K || !can_gather || (opts && opts->tile_t == 240)))
     return VENOM_ERR_INVALID_ARGUMENT;
   const bool has_tc = opts && opts->metadata_tc;
   // metadata is not read with pre-ordered metadata; column_idx is not read when M = 4 (identity)
@@ -538,12 +541,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
 
   if (K == 0) {
     const int64_t n = R * T;
-    if (bf16)
-      venom::vnm_fill_bias_kernel<true><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-          static_cast<uint16_t*>(C), R, T, ldc, static_cast<const uint16_t*>(bias));
-    else
-      venom::vnm_fill_bias_kernel<false><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-          static_cast<uint16_t*>(C), R, T, ldc, static_cast<const uint16_t*>(bias));
+    venom::vnm_fill_bias_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        static_cast<uint16_t*>(C), R, T, ldc, static_cast<const uint16_t*>(bias), ct ? 1 : 0);
     return launch_status();
   }
 
@@ -578,6 +577,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.m_tiles = static_cast<int>((R + 127) / 128);
   p.is_bf16 = bf16;
   p.b3d = 0;
+  p.c_t = ct ? 1 : 0;
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -641,7 +641,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     // 512 × 240 pair tiles (two accumulators per CTA) land 1.45× fewer bytes per FLOP but expose a
     // larger last epilogue: measured better only with long k-loops and at least one full wave of
     // pair tiles
-    if (contiguous && pair == 2 && opts && opts->metadata_tc) {
+    if (contiguous && pair == 2 && opts && opts->metadata_tc && !ct) {
       int sms = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

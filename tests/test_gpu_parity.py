@@ -677,3 +677,38 @@ def test_spmm_degenerate_shapes():
     xr = venom.compress(torch.empty((0, 64), dtype=torch.float16, device="cuda"), V=64, M=8)
     assert venom.spmm(xr, torch.randn(64, 16, device="cuda").half()).shape == (0, 16)
     assert venom.spmm(x, torch.empty((K, 0), dtype=torch.float16, device="cuda")).shape == (R, 0)
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,bias", [
+    (192, 640, 136, 64, 10, F16, True),    # encoder's 64:2:10 (gathered, two V-blocks per tile)
+    (384, 1024, 200, 128, 16, BF16, False),
+    (512, 1024, 264, 128, 4, F16, True),   # 2:4 (contiguous, CTA pair)
+    (130, 256, 64, 13, 8, F16, True),      # dense-K-only V -> rejected for token-major C
+])
+def test_spmm_transposed_output(R, K, T, V, M, dt, bias):
+    """Token-major C^T (opts.c_transposed): bitwise the transpose of the row-major result (same
+    accumulation and rounding) and within tolerance of the oracle; unsupported paths are refused."""
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 800 + R + T + M, bias)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = vnm_from(parts, R, K, V, M, dt)
+    bd = to_dev(bv, dt) if bias else None
+    can = (M == 4 or V in (32, 64) or V % 128 == 0) and (K // M) % 4 == 0
+    if not can:
+        with pytest.raises(venom.VenomError) as ei:
+            venom.spmm(x, to_dev(B, dt), bias=bd, transposed_out=True)
+        assert ei.value.status == 1
+        return
+    for pre in (False, True):
+        if pre:
+            venom.order_metadata(x)
+        C = venom.spmm(x, to_dev(B, dt), bias=bd)
+        Ct = venom.spmm(x, to_dev(B, dt), bias=bd, transposed_out=True)
+        assert Ct.shape == (T, R)
+        assert torch.equal(Ct.t(), C)
+        check_spmm(Ct.t().contiguous(), C_ref, dt)
+    # a wider leading dimension (a column slice of a [T, 3R] buffer, as the encoder's QKV uses)
+    buf = torch.full((T, R + 64), float("nan"), dtype=tdt(dt), device="cuda")
+    venom.spmm(x, to_dev(B, dt), bias=bd, transposed_out=True, out=buf[:, :R])
+    assert torch.equal(buf[:, :R].t(), C) and torch.isnan(buf[:, R:]).all()
+    with pytest.raises(venom.VenomError):
+        venom.spmm(x, to_dev(B, dt), bias=bd, transposed_out=True, strategy=venom.STRATEGY_DENSE_K)
