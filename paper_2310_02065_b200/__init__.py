@@ -33,7 +33,9 @@ EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "ven
             "venom_spmm_ex", "venom_expand_2to4", "venom_compress_2to4", "venom_prefer_2to4",
             "venom_metadata_tc_bytes",
             "venom_order_metadata", "venom_kernels_per_call", "venom_status_string",
-            "venom_version", "venom_compress_masked", "venom_energy"]
+            "venom_version", "venom_compress_masked", "venom_energy",
+            # include/venom_encoder.h (encoder layout helpers, not the V:N:M method)
+            "venom_enc_add_layernorm", "venom_enc_heads_to_fm"]
 
 
 class VenomError(RuntimeError):
@@ -81,6 +83,8 @@ def lib() -> ctypes.CDLL:
         L.venom_compress_2to4.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P, P, P]
         L.venom_compress_masked.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, _Format, P, P, P, P, P]
         L.venom_energy.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, P, P]
+        L.venom_enc_add_layernorm.argtypes = [P, P, P, P, I64, I64, ctypes.c_float, ctypes.c_int, P, P, I64, P]
+        L.venom_enc_heads_to_fm.argtypes = [P, I64, I64, I64, I64, I64, I64, I64, ctypes.c_int, P, I64, P]
         L.venom_prefer_2to4.restype = ctypes.c_int
         L.venom_spmm_ex.argtypes = [P, P, P, I64, I64, _Format, P, I64, I64, P, I64, P, ctypes.c_int,
                                     ctypes.POINTER(_Opts), P]
@@ -221,6 +225,34 @@ def energy(A: torch.Tensor, kept: "VNMTensor | torch.Tensor", out: Optional[torc
                             ctypes.c_void_p(out.data_ptr()), _stream(A.device))
     _check(st, "venom_energy")
     return out
+
+
+def enc_add_layernorm(x: torch.Tensor, y: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float,
+                      out_tm: torch.Tensor, out_fm: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Encoder helper (include/venom_encoder.h): out_tm = LayerNorm(x + y) token-major [T, h], and
+    the same values feature-major into out_fm [h, >= T] (row stride may exceed T)."""
+    T, h = x.shape
+    for t in (x, y, out_tm):
+        assert t.is_contiguous() and t.shape == (T, h) and t.dtype == x.dtype
+    if out_fm is not None:
+        assert out_fm.stride(1) == 1 and out_fm.shape[0] >= h and out_fm.shape[1] >= T  # rows >= h untouched
+    _check(lib().venom_enc_add_layernorm(
+        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+        ctypes.c_void_p(b.data_ptr()), T, h, float(eps), _dt(x.dtype), ctypes.c_void_p(out_tm.data_ptr()),
+        ctypes.c_void_p(out_fm.data_ptr() if out_fm is not None else 0),
+        out_fm.stride(0) if out_fm is not None else 0, _stream(x.device)), "venom_enc_add_layernorm")
+    return out_tm
+
+
+def enc_heads_to_fm(a: torch.Tensor, out_fm: torch.Tensor) -> torch.Tensor:
+    """Encoder helper: attention output a [B, H, S, D] (any strides, D contiguous) -> feature-major
+    out_fm[h*D + d, b*S + s]."""
+    B_, H_, S_, D_ = a.shape
+    assert a.stride(3) == 1 and out_fm.stride(1) == 1
+    _check(lib().venom_enc_heads_to_fm(
+        ctypes.c_void_p(a.data_ptr()), B_, H_, S_, D_, a.stride(0), a.stride(1), a.stride(2), _dt(a.dtype),
+        ctypes.c_void_p(out_fm.data_ptr()), out_fm.stride(0), _stream(a.device)), "venom_enc_heads_to_fm")
+    return out_fm
 
 
 def decompress(x: VNMTensor, out: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None,

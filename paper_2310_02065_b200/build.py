@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libvenom.so")
 SOURCES = [os.path.join(HERE, "csrc", "venom_api.cu")]
 DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
-    [os.path.join(ROOT, "include", "venom.h")]
+    sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]

@@ -9,9 +9,11 @@
 #include <mutex>
 
 #include "../../include/venom.h"
+#include "../../include/venom_encoder.h"
 #include "format_kernels.cuh"
 #include "densek_kernel.cuh"
 #include "spmm_kernel.cuh"
+#include "encoder_kernels.cuh"
 
 namespace {
 
@@ -719,3 +721,60 @@ venom_status_t venom_spmm(const void* values, const uint8_t* metadata, const uin
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ encoder layout kernels
+// (include/venom_encoder.h; SURVEY §8(f) rank 1 plumbing, not the V:N:M method)
+extern "C" venom_status_t venom_enc_add_layernorm(const void* x, const void* y, const void* w, const void* b,
+                                                  int64_t T, int64_t h, float eps, venom_dtype_t dt,
+                                                  void* out_tm, void* out_fm, int64_t ld_fm,
+                                                  venom_stream_t stream) {
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (!x || !y || !w || !b || !out_tm || T < 0 || h % 256 != 0 || h <= 0 || h > 1024 || T % 32 != 0)
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (out_fm && (ld_fm < T || ld_fm % 8 != 0)) return VENOM_ERR_INVALID_ARGUMENT;
+  if (!aligned(x, 16) || !aligned(y, 16) || !aligned(w, 16) || !aligned(b, 16) || !aligned(out_tm, 16))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (T == 0) return VENOM_OK;
+  venom_status_t st = check_arch();
+  if (st != VENOM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nv = static_cast<int>(h / 256);
+  const int smem = static_cast<int>(32 * (h + 2) * 2);
+  const unsigned grid = static_cast<unsigned>(T / 32);
+  auto go = [&](auto kern) -> venom_status_t {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return VENOM_ERR_CUDA;
+    kern<<<grid, 256, smem, s>>>(static_cast<const uint16_t*>(x), static_cast<const uint16_t*>(y),
+                                 static_cast<const uint16_t*>(w), static_cast<const uint16_t*>(b), T, eps,
+                                 static_cast<uint16_t*>(out_tm), static_cast<uint16_t*>(out_fm), ld_fm);
+    return launch_status();
+  };
+  const bool bf = dt == VENOM_BF16;
+  switch (nv) {
+    case 1: return bf ? go(venom::vnm_enc_add_layernorm_kernel<true, 1>) : go(venom::vnm_enc_add_layernorm_kernel<false, 1>);
+    case 2: return bf ? go(venom::vnm_enc_add_layernorm_kernel<true, 2>) : go(venom::vnm_enc_add_layernorm_kernel<false, 2>);
+    case 3: return bf ? go(venom::vnm_enc_add_layernorm_kernel<true, 3>) : go(venom::vnm_enc_add_layernorm_kernel<false, 3>);
+    default: return bf ? go(venom::vnm_enc_add_layernorm_kernel<true, 4>) : go(venom::vnm_enc_add_layernorm_kernel<false, 4>);
+  }
+}
+
+extern "C" venom_status_t venom_enc_heads_to_fm(const void* a, int64_t B, int64_t H, int64_t S, int64_t D,
+                                                int64_t sb, int64_t sh, int64_t ss, venom_dtype_t dt,
+                                                void* out_fm, int64_t ld_fm, venom_stream_t stream) {
+  if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
+  if (!a || !out_fm || B < 0 || H < 0 || D != 64 || S % 64 != 0 || ld_fm < B * S || ld_fm % 8 != 0 ||
+      sb % 8 != 0 || sh % 8 != 0 || ss % 8 != 0 || !aligned(a, 16) || !aligned(out_fm, 4))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (B * H * S == 0) return VENOM_OK;
+  venom_status_t st = check_arch();
+  if (st != VENOM_OK) return st;
+  const unsigned grid = static_cast<unsigned>(B * H * (S / 64));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dt == VENOM_BF16)
+    venom::vnm_enc_heads_to_fm_kernel<true><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), H, S, sb, sh,
+                                                                 ss, static_cast<uint16_t*>(out_fm), ld_fm);
+  else
+    venom::vnm_enc_heads_to_fm_kernel<false><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), H, S, sb, sh,
+                                                                  ss, static_cast<uint16_t*>(out_fm), ld_fm);
+  return launch_status();
+}

@@ -4,10 +4,13 @@ BASELINE.json configs[4]: every linear layer V:N:M 64:2:10, batch 32 × seq 512)
 The four linear layers of each encoder layer (QKV 3072×1024, attention output 1024×1024, FFN1
 4096×1024, FFN2 1024×4096) run as V:N:M SpMMs through the C ABI; attention (torch SDPA),
 GELU, residual adds and LayerNorm stay dense in torch, as in the paper's STen integration
-(PAPER.md:443-474). Activations are kept FEATURE-MAJOR ([features, tokens]) end to end, so each
-sparse layer's output is directly the next one's B operand (reading #14). K is padded
-to a multiple of 8·M with zero weight columns and zero activation rows (reading #11): the padded
-activation buffers are allocated once with zero tails and the producers write only the real rows.
+(PAPER.md:443-474). The SpMM's B operand is feature-major ([features, tokens], DESIGN.md reading
+#14); its output is written feature-major where the next op is another SpMM (FFN1 -> GELU -> FFN2)
+and token-major (``transposed_out``) where attention or LayerNorm reads it (QKV, attention
+output, FFN2), so the residual stream stays token-major as in the dense model and only the three
+B operands that follow a token-major op (x, the attention output, the post-LN x1) are transposed.
+K is padded to a multiple of 8·M with zero weight columns and zero activation rows (reading #11):
+the padded activation buffers are allocated once with zero tails and only the real rows are written.
 
 This module is a user of the library, not part of the hot path: every SpMM is venom_spmm; the
 dense parts are plain torch ops.
@@ -21,7 +24,8 @@ from typing import List, Optional
 import torch
 import torch.nn.functional as F
 
-from . import VNMTensor, compress, compress_2to4, order_metadata, prefers_2to4, spmm
+from . import (VNMTensor, compress, compress_2to4, enc_add_layernorm, enc_heads_to_fm, order_metadata,
+               prefers_2to4, spmm)
 
 
 def padded(k: int, M: int) -> int:
@@ -47,9 +51,10 @@ class SparseLinear:
             self.op = order_metadata(self.x)
         self.bias = bias
 
-    def __call__(self, x_fm: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def __call__(self, x_fm: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 token_major: bool = False) -> torch.Tensor:
         assert x_fm.shape[0] == self.K, (x_fm.shape, self.K)
-        return spmm(self.op, x_fm, bias=self.bias, out=out)
+        return spmm(self.op, x_fm, bias=self.bias, out=out, transposed_out=token_major)
 
 
 @dataclass
@@ -108,15 +113,15 @@ class SparseEncoder:
                 L[k] = lw[k]
             self.layers.append(L)
         L0 = self.layers[0]
-        # feature-major activation buffers with zero K-padding rows (written only in [:real rows])
-        self.x_in = torch.zeros((L0["qkv"].K, T), dtype=dt, device=dev)
-        self.attn = torch.zeros((L0["o"].K, T), dtype=dt, device=dev)
-        self.x1 = torch.zeros((L0["f1"].K, T), dtype=dt, device=dev)
+        # feature-major B operands with zero K-padding rows (written only in [:real rows])
+        self.x_fm = torch.zeros((L0["qkv"].K, T), dtype=dt, device=dev)
+        self.attn_fm = torch.zeros((L0["o"].K, T), dtype=dt, device=dev)
+        self.x1_fm = torch.zeros((L0["f1"].K, T), dtype=dt, device=dev)
         self.hid = torch.zeros((L0["f2"].K, T), dtype=dt, device=dev)
-        self.qkv = torch.empty((3 * cfg.hidden, T), dtype=dt, device=dev)
-        self.o = torch.empty((cfg.hidden, T), dtype=dt, device=dev)
-        self.f1 = torch.empty((cfg.ffn, T), dtype=dt, device=dev)
-        self.f2 = torch.empty((cfg.hidden, T), dtype=dt, device=dev)
+        # token-major SpMM outputs (transposed_out) and the feature-major FFN1 output
+        self.qkv_tm = torch.empty((T, 3 * cfg.hidden), dtype=dt, device=dev)
+        self.o_tm = torch.empty((T, cfg.hidden), dtype=dt, device=dev)
+        self.f2_tm = torch.empty((T, cfg.hidden), dtype=dt, device=dev)
 
     def dense_weights(self) -> List[dict]:
         from . import decompress
@@ -133,39 +138,38 @@ class SparseEncoder:
 
     def forward(self, x_tm: torch.Tensor) -> torch.Tensor:
         """x_tm: [tokens, hidden] (token-major, as a user holds it); returns the same layout."""
-        cfg = self.cfg
-        h = cfg.hidden
-        self.x_in[:h].copy_(x_tm.t())
-        x = self.x_in
+        h = self.cfg.hidden
+        self.x_fm[:h].copy_(x_tm.t())  # the first layer's B operand; later ones come from LayerNorm
+        x = x_tm
         for L in self.layers:
-            x = self._layer(L, x)  # self.x1: the layer output, K-padded like the input
-        return x[:h].t().contiguous()
+            x = self._layer(L, x)
+        return x
 
-    def _attention(self, qkv_fm: torch.Tensor, out_fm: torch.Tensor):
+    def _attention(self, qkv_tm: torch.Tensor, out_fm: torch.Tensor):
         cfg = self.cfg
         Bt, S, H = cfg.batch, cfg.seq, cfg.heads
-        D = cfg.hidden // H
-        # feature-major [3h, T] -> token-major once, then [B, H, S, D] views for SDPA (flash)
-        qkv = qkv_fm.t().contiguous()
-        q, k, v = (qkv[:, i * cfg.hidden:(i + 1) * cfg.hidden].view(Bt, S, H, D).transpose(1, 2)
-                   for i in range(3))
+        h = cfg.hidden
+        D = h // H
+        # token-major [T, 3h] straight from the QKV SpMM: [B, H, S, D] views for SDPA (flash)
+        q, k, v = (qkv_tm[:, i * h:(i + 1) * h].view(Bt, S, H, D).transpose(1, 2) for i in range(3))
         a = F.scaled_dot_product_attention(q, k, v)  # [B, H, S, D]
-        out_fm[:cfg.hidden].copy_(a.transpose(1, 2).reshape(Bt * S, cfg.hidden).t())
+        enc_heads_to_fm(a, out_fm)  # the O projection's B operand, feature-major [h, T]
 
     def _layer(self, L: dict, x: torch.Tensor) -> torch.Tensor:
         cfg = self.cfg
         h = cfg.hidden
-        L["qkv"](x, out=self.qkv)
-        self._attention(self.qkv, self.attn)
-        L["o"](self.attn, out=self.o)
-        y = F.layer_norm((x[:h] + self.o).t(), (h,), L["ln1_w"], L["ln1_b"], cfg.eps)  # [T, h]
-        self.x1[:h].copy_(y.t())
-        L["f1"](self.x1, out=self.f1)
-        self.hid[:cfg.ffn].copy_(F.gelu(self.f1))
-        L["f2"](self.hid, out=self.f2)
-        z = F.layer_norm((self.x1[:h] + self.f2).t(), (h,), L["ln2_w"], L["ln2_b"], cfg.eps)
-        self.x1[:h].copy_(z.t())
-        return self.x1
+        # x: token-major residual stream; self.x_fm: the same values feature-major (QKV's B)
+        L["qkv"](self.x_fm, out=self.qkv_tm, token_major=True)
+        self._attention(self.qkv_tm, self.attn_fm)
+        L["o"](self.attn_fm, out=self.o_tm, token_major=True)
+        x1 = torch.empty_like(x)
+        enc_add_layernorm(x, self.o_tm, L["ln1_w"], L["ln1_b"], cfg.eps, x1, self.x1_fm)
+        f1 = L["f1"](self.x1_fm, out=self.hid[:cfg.ffn])                      # [4h, T], FFN2's B
+        torch.ops.aten.gelu_(f1)                                               # in place
+        L["f2"](self.hid, out=self.f2_tm, token_major=True)
+        out = torch.empty_like(x)
+        enc_add_layernorm(x1, self.f2_tm, L["ln2_w"], L["ln2_b"], cfg.eps, out, self.x_fm)
+        return out
 
 
 def dense_forward(cfg: EncoderConfig, dense: List[dict], x_tm: torch.Tensor) -> torch.Tensor:

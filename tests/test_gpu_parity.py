@@ -712,3 +712,29 @@ def test_spmm_transposed_output(R, K, T, V, M, dt, bias):
     assert torch.equal(buf[:, :R].t(), C) and torch.isnan(buf[:, R:]).all()
     with pytest.raises(venom.VenomError):
         venom.spmm(x, to_dev(B, dt), bias=bd, transposed_out=True, strategy=venom.STRATEGY_DENSE_K)
+
+
+def test_encoder_layout_helpers():
+    """include/venom_encoder.h: add+LayerNorm (token-major out within 1 ulp of torch's fp32-internal
+    layer_norm, feature-major copy bitwise its transpose) and the attention-output transpose (exact)."""
+    torch.manual_seed(5)
+    for dt in (torch.float16, torch.bfloat16):
+        T, h = 96, 1024
+        x = torch.randn(T, h, device="cuda").to(dt)
+        y = torch.randn(T, h, device="cuda").to(dt)
+        w = (1 + 0.1 * torch.randn(h, device="cuda")).to(dt)
+        b = (0.1 * torch.randn(h, device="cuda")).to(dt)
+        out = torch.empty_like(x)
+        fm = torch.full((h, T + 8), float("nan"), dtype=dt, device="cuda")
+        venom.enc_add_layernorm(x, y, w, b, 1e-12, out, fm)
+        ref = torch.nn.functional.layer_norm((x.float() + y.float()), (h,), w.float(), b.float(), 1e-12)
+        ulp = 2.0 ** -10 if dt == torch.float16 else 2.0 ** -7
+        assert ((out.float() - ref).abs() <= ulp * ref.abs() + 1e-3).all()
+        assert torch.equal(fm[:, :T], out.t()) and torch.isnan(fm[:, T:]).all()
+        # attention output [B, H, S, D], also as a transposed view ([B, S, H, D] storage)
+        Bt, H, S, D = 2, 4, 128, 64
+        for a in (torch.randn(Bt, H, S, D, device="cuda").to(dt),
+                  torch.randn(Bt, S, H, D, device="cuda").to(dt).transpose(1, 2)):
+            o = torch.empty((H * D, Bt * S), dtype=dt, device="cuda")
+            venom.enc_heads_to_fm(a, o)
+            assert torch.equal(o, a.permute(1, 3, 0, 2).reshape(H * D, Bt * S))
