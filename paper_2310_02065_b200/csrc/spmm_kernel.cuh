@@ -240,7 +240,7 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 // TMEM -> +bias (fp32) -> RNE to fp16/bf16 packed in registers; the accumulator buffer is released
 // to the MMA warp as soon as it has been read, and the 16-byte global stores overlap the next
 // tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
-template <class Cfg, bool kBF16, int CG = 1>
+template <class Cfg, bool kBF16, int CG = 1, bool kCT = false>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane,
                                               uint32_t stage_smem = 0) {
@@ -289,7 +289,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       else mbar_arrive(acce0 + 8 * ab);
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
-    if (p.c_t) {
+    if constexpr (kCT) {
       // token-major C (C^T[t][r]): for each column t the warp's 32 lanes hold 32 consecutive rows,
       // so one 16-bit store per lane writes 64 contiguous bytes of C^T row t — coalesced as is
       if (row < p.R) {
@@ -504,7 +504,7 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
   }
 }
 
-template <class Cfg, bool kBF16, bool kContig>
+template <class Cfg, bool kBF16, bool kContig, bool kCT>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
-    else epilogue_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
+    else epilogue_role<Cfg, kBF16, CG, kCT>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
