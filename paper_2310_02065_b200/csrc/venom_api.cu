@@ -478,10 +478,11 @@ int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f) {
   if ((K / 4) % 4 != 0 || T < 256) return 0;
   // the fused preparation (venom_compress_2to4) must apply
   if (f.m % 8 != 0 || 128 % f.m != 0 || f.v % 16 != 0 || f.v > 256 || K % 16 != 0) return 0;
-  // measured crossover: the gathered path is bound by the gather feed,
-  // whose bytes per useful FLOP grow as 1/V, while the 2:4 CTA-pair path streams dense B tiles
-  // at twice the useful work; below V·M ≈ 1536 the 2:4 form wins
-  return static_cast<int64_t>(f.v) * f.m <= 1536 ? 1 : 0;
+  // measured crossover (profiles/r01_vscaling_sweep.txt, 4096³ for V in
+  // {32, 64, 128, 256} and M in {8, 16, 32}): the gathered path lands bytes per useful FLOP that
+  // fall with V and M, while the V:2:4 form's time does not depend on V or M; the V:2:4 form wins
+  // for M = 8 at every V, and for V·M <= 1024 otherwise
+  return (f.m <= 8 || static_cast<int64_t>(f.v) * f.m <= 1024) ? 1 : 0;
 }
 
 venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,

@@ -29,6 +29,13 @@ WORKLOADS = {
     "sweep_4096x4096x4096_64:2:8": dict(R=4096, K=4096, T=4096, V=64, M=8, cfg=2),
     "sweep_4096x4096x4096_64:2:16": dict(R=4096, K=4096, T=4096, V=64, M=16, cfg=2),
     "sweep_4096x4096x4096_64:2:32": dict(R=4096, K=4096, T=4096, V=64, M=32, cfg=2),
+    # V-scaling study (the paper's Fig 8 axis): V in {32, 256}
+    "sweep_4096x4096x4096_32:2:8": dict(R=4096, K=4096, T=4096, V=32, M=8, cfg=2),
+    "sweep_4096x4096x4096_32:2:16": dict(R=4096, K=4096, T=4096, V=32, M=16, cfg=2),
+    "sweep_4096x4096x4096_32:2:32": dict(R=4096, K=4096, T=4096, V=32, M=32, cfg=2),
+    "sweep_4096x4096x4096_256:2:8": dict(R=4096, K=4096, T=4096, V=256, M=8, cfg=2),
+    "sweep_4096x4096x4096_256:2:16": dict(R=4096, K=4096, T=4096, V=256, M=16, cfg=2),
+    "sweep_4096x4096x4096_256:2:32": dict(R=4096, K=4096, T=4096, V=256, M=32, cfg=2),
     "sweep_4096x4160x4096_64:2:40": dict(R=4096, K=4160, T=4096, V=64, M=40, cfg=2),
     # the paper's Fig 6 family: BERT-large-shaped 1024×K×4096 at V = 128,
     # N:M = 2:10 / 2:20 / 2:40 / 2:100 (K padded to a multiple of 8M, reading #11)

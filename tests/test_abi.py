@@ -147,3 +147,11 @@ def test_no_cpu_fallback_without_device(L):
     p = P(ctypes.addressof(buf) + (16 - ctypes.addressof(buf) % 16) % 16)
     st = L.venom_spmm(p, p, p, 128, 128, venom._Format(64, 2, 8), p, 8, 8, p, 8, P(0), 0, P(0))
     assert st in (8, 9)
+
+
+@pytest.mark.parametrize("V,M,expect", [(32, 8, 1), (256, 8, 1), (64, 16, 1), (128, 16, 0), (256, 16, 0),
+                                        (32, 32, 1), (64, 32, 0), (128, 4, 0), (64, 10, 0)])
+def test_planner_operand_form(L, V, M, expect):
+    """venom_prefer_2to4 follows the measured V-scaling crossover (DESIGN.md planner table): the
+    V:2:4 form for M = 8 or V·M <= 1024; never for M = 4 (already 2:4) or M % 4 != 0."""
+    assert L.venom_prefer_2to4(4096, 4096 if M != 10 else 4160, 4096, venom._Format(V, 2, M)) == expect
