@@ -223,6 +223,11 @@ typedef struct {
                         a PyTorch [tokens, features] activation use. Gathered / contiguous kernel
                         with one 128-row accumulator per CTA only (tile_t 240 and DENSE_K are
                         rejected with VENOM_ERR_INVALID_ARGUMENT). 0: row-major C (default). */
+  int32_t b_kmajor;    /* 1: B is given K-major (token-major activations, the PyTorch [tokens,
+                        features] layout): dtype[T][ldb] with ldb >= K, ldb % 8 == 0. M = 4 operands
+                        only (plain 2:4 or the V:2:4 form of venom_compress_2to4), one accumulator per
+                        CTA (tile_t 240 and DENSE_K rejected). With c_transposed this is
+                        Y = X·Wᵀ on [T, K] activations. 0: B row-major dtype[K][ldb] (default). */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

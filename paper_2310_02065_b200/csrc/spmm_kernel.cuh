@@ -48,6 +48,7 @@ struct SpmmParams {
   int is_bf16;
   int b3d;  // M = 4: B map is 3-D [T/64][K][64] (one box per stage) instead of 2-D
   int c_t;  // C stored transposed (token-major): element (r, t) at C[t * ldc + r]
+  int bk;   // B given K-major (token-major activations, dtype[T][ldb]); M = 4 operand only
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -161,13 +162,14 @@ __device__ __forceinline__ int my_tile_count(const SpmmParams& p) {
 // MMA issuer (one elected lane of the pair leader): per k-stage, 4 sparse MMAs (K = 32) per
 // V-block. Stage layout: [A 16 KB K-major SW128][NB × B' (BNH/64 chunks × 16 KB, MN-major SW128)];
 // the stage's metadata sits in TMEM columns E_COL + 4·stage (written by the metadata warps).
-template <class Cfg, bool kBF16, int CG = 1>
+template <class Cfg, bool kBF16, int CG = 1, bool kBK = false>
 __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                          uint32_t smem0, uint32_t full0, uint32_t empty0,
                                          uint32_t accf0, uint32_t acce0, int lane) {
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
-  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128 * CG, BN);
+  // kBK: B' is K-major (bit 16 clear), else MN-major
+  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128 * CG, BN) & (kBK ? ~(1u << 16) : ~0u);
   for (int tl = 0; tl < my_tiles; ++tl) {
     const int ab = tl % Cfg::ACC_BUFS;
     const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
@@ -206,8 +208,11 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
             const uint64_t adesc = smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + kb * 32, 16, 1024, 2);
             // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
             // K advance 32 rows = 4096 B per MMA
-            const uint64_t bdesc = smem_desc(sbase + Cfg::A_BYTES + (NB > 1 ? b * Cfg::B_BYTES : 0) + kb * 4096,
-                                             Cfg::B_CHUNK, 1024, 2);
+            // kBK: two K-major SW128 regions of BNH rows × 64 K-elements; K = 32 per MMA = 64 B
+            const uint64_t bdesc =
+                kBK ? smem_desc(sbase + Cfg::A_BYTES + (kb >> 1) * (Cfg::BNH * 128) + (kb & 1) * 64, 16, 1024, 2)
+                    : smem_desc(sbase + Cfg::A_BYTES + (NB > 1 ? b * Cfg::B_BYTES : 0) + kb * 4096,
+                                Cfg::B_CHUNK, 1024, 2);
             if constexpr (CG == 2)
               tc_mma_sp_f16_2sm(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
                                 (ks | kb) != 0 ? 1u : 0u);
@@ -432,7 +437,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
 // lane 0 of warp 1 the B' box (one 3-D box, or one 2-D box per 64-column chunk on warps 1..NCH).
 // Tile coordinates advance incrementally: the whole per-stage cost is a barrier wait and a few
 // instructions (the generic per-stage coordinate computation took longer than the stage's MMAs).
-template <class Cfg>
+template <class Cfg, bool kBK = false>
 __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const CUtensorMap* tm_values,
                                                     const CUtensorMap* tm_b, const CUtensorMap* tm_e,
                                                     int my_tiles, uint32_t smem0, uint32_t full0,
@@ -440,7 +445,7 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, CG = Cfg::CG, MB = Cfg::MB;
   const bool b3d = p.b3d != 0;
-  const int role = warp == 0 ? 0 : ((b3d ? warp == 1 : warp <= Cfg::NCH) ? 1 : -1);
+  const int role = warp == 0 ? 0 : (((b3d || kBK) ? warp == 1 : warp <= Cfg::NCH) ? 1 : -1);
   if (role < 0 || my_tiles == 0) return;
   const uint64_t pol_a = policy_evict_first();
   const uint64_t pol_b = policy_evict_last();
@@ -483,7 +488,15 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
         }
       VENOM_TRACE_EVENT(4, it);
     } else if (do_b) {
-      if (b3d) {
+      if constexpr (kBK) {
+        // K-major B ([T][K]): two boxes of BNH token rows × 64 K-elements (K-major SW128)
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          const uint32_t bdst = sbase + Cfg::A_BYTES + kc * (Cfg::BNH * 128);
+          if constexpr (CG == 2) tma_load_2d_2sm(bdst, tm_b, fbar, ks * 128 + 64 * kc, col0, pol_b);
+          else tma_load_2d(bdst, tm_b, fbar, ks * 128 + 64 * kc, col0, pol_b);
+        }
+      } else if (b3d) {
         if constexpr (CG == 2) tma_load_3d_2sm(sbase + Cfg::A_BYTES, tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
         else tma_load_3d(sbase + Cfg::A_BYTES, tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
       } else {
@@ -504,7 +517,7 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
   }
 }
 
-template <class Cfg, bool kBF16, bool kContig, bool kCT>
+template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
 
   if (warp < Cfg::P && kContig) {
     if (lane == 0)
-      producer_contiguous<Cfg>(p, &tm_values, &tm_b, &tm_e, my_tiles, smem0, full0, empty0, rank, warp);
+      producer_contiguous<Cfg, kBK>(p, &tm_values, &tm_b, &tm_e, my_tiles, smem0, full0, empty0, rank, warp);
   } else if (warp < Cfg::P) {
     // ======================= producers: values tile + gathered B' rows =======================
     // Stage ops are (block b, chunk c, group q); warp w issues ops [w·OPS_PER_WARP, ...), one per
@@ -691,7 +704,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
       }
     }
   } else if (warp == Cfg::W_MMA) {
-    if (rank == 0) mma_role<Cfg, kBF16, CG>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
+    if (rank == 0) mma_role<Cfg, kBF16, CG, kBK>(p, my_tiles, tmem_base, smem0, full0, empty0, accf0, acce0, lane);
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);

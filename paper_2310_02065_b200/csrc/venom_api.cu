@@ -113,6 +113,13 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUte
                                 : venom::vnm_spmm_kernel<Cfg, kBF16, false, true>)
                     : (p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, false>
                                 : venom::vnm_spmm_kernel<Cfg, kBF16, false, false>);
+  if constexpr (Cfg::MB == 1 && Cfg::NB == 1 && Cfg::BNH % 64 == 0) {
+    // K-major B (token-major activations): M = 4 operand only (checked by the caller)
+    if (p.bk) kern = p.c_t ? venom::vnm_spmm_kernel<Cfg, kBF16, true, true, true>
+                           : venom::vnm_spmm_kernel<Cfg, kBF16, true, false, true>;
+  } else {
+    if (p.bk) return VENOM_ERR_INVALID_ARGUMENT;
+  }
   // >= 116 KB of shared memory guarantees one CTA per SM (each CTA allocates all 512 TMEM columns)
   const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -530,11 +537,14 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (strategy < 0 || strategy > 2) return VENOM_ERR_INVALID_ARGUMENT;
   if (!can_gather && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
   const bool ct = opts && opts->c_transposed;  // token-major C^T[T][ldc]
+  const bool bk = opts && opts->b_kmajor;      // token-major B[T][ldb]
   if (T < 0) return VENOM_ERR_INVALID_ARGUMENT;
   if (R == 0 || T == 0) return VENOM_OK;  // nothing to compute (leading dimensions are then moot)
-  if (ldb < T || (ct ? ldc < R : ldc < T) || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
+  if ((bk ? ldb < K : ldb < T) || (ct ? ldc < R : ldc < T) || T % 8 != 0 || ldb % 8 != 0 || ldc % 8 != 0)
     return VENOM_ERR_INVALID_ARGUMENT;
   if (ct && (strategy == VENOM_STRATEGY_DENSE_K || !can_gather || (opts && opts->tile_t == 240)))
+    return VENOM_ERR_INVALID_ARGUMENT;
+  if (bk && (f.m != 4 || strategy == VENOM_STRATEGY_DENSE_K || (opts && opts->tile_t == 240) || K % 8 != 0))
     return VENOM_ERR_INVALID_ARGUMENT;
   const bool has_tc = opts && opts->metadata_tc;
   // metadata is not read with pre-ordered metadata; column_idx is not read when M = 4 (identity)
@@ -585,7 +595,9 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.m_tiles = static_cast<int>((R + 127) / 128);
   p.is_bf16 = bf16;
   p.b3d = 0;
+  p.bk = 0;
   p.c_t = ct ? 1 : 0;
+  p.bk = bk ? 1 : 0;
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -649,7 +661,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     // 512 × 240 pair tiles (two accumulators per CTA) land 1.45× fewer bytes per FLOP but expose a
     // larger last epilogue: measured better only with long k-loops and at least one full wave of
     // pair tiles
-    if (contiguous && pair == 2 && opts && opts->metadata_tc && !ct) {
+    if (contiguous && pair == 2 && opts && opts->metadata_tc && !ct && !bk) {
       int sms = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -659,7 +671,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   }
   set_tiles(tile_t);
   (void)stages;
-  p.b3d = contiguous && (T % 64 == 0) && ((tile_t / pair) % 64 == 0);
+  p.b3d = contiguous && !bk && (T % 64 == 0) && ((tile_t / pair) % 64 == 0);
   if (p.b3d) {
     const int nch = (tile_t / pair + 63) / 64;
     cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(T / 64)};
@@ -671,7 +683,21 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       p.b3d = 0;  // driver refused the chunk-stride map: 2-D boxes below
   }
-  if (!p.b3d && !encode_b(&tb, contiguous ? 128 : 1)) return VENOM_ERR_CUDA;
+  if (bk) {
+    // K-major B: 2-D [T rows][K] with a box of BNH token rows × 64 K-elements (K-major SW128)
+    const int bnh = tile_t / pair;
+    if (bnh % 64 != 0) return VENOM_ERR_INVALID_ARGUMENT;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(T)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldb)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(bnh)};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(B), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  } else if (!p.b3d && !encode_b(&tb, contiguous ? 128 : 1)) {
+    return VENOM_ERR_CUDA;
+  }
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
   if (meta_tc == nullptr) return run_gather<false>(NBg, pair, tile_t, bf16, tv, tb, tv, p, max_ctas, s);
   // pre-ordered metadata: the [tiles·num_ks] contiguous 2 KB stage blocks, mapped as 2-D

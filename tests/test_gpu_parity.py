@@ -738,3 +738,44 @@ def test_encoder_layout_helpers():
             o = torch.empty((H * D, Bt * S), dtype=dt, device="cuda")
             venom.enc_heads_to_fm(a, o)
             assert torch.equal(o, a.permute(1, 3, 0, 2).reshape(H * D, Bt * S))
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,bias,tile_t,pair", [
+    (512, 1024, 512, 128, 4, F16, True, 256, 0),   # 2:4, CTA pair 256 x 256
+    (384, 640, 264, 64, 4, BF16, False, 128, 0),   # pair 256 x 128, ragged R and T
+    (256, 512, 256, 128, 4, F16, True, 256, 1),    # one CTA per 128 rows, 256 columns
+])
+def test_spmm_kmajor_b(R, K, T, V, M, dt, bias, tile_t, pair):
+    """K-major B (opts.b_kmajor, token-major activations [T, K]): bitwise the row-major-B result
+    (the MMA reads the same values in the same K order), for row-major and token-major C."""
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 900 + R + T, bias)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = vnm_from(parts, R, K, V, M, dt)
+    bd = to_dev(bv, dt) if bias else None
+    Bd = to_dev(B, dt)
+    Bt = Bd.t().contiguous()  # [T, K]
+    for pre in (False, True):
+        if pre:
+            venom.order_metadata(x)
+        kw = dict(bias=bd, tile_t=tile_t, cta_pair=pair, strategy=venom.STRATEGY_GATHER)
+        C = venom.spmm(x, Bd, **kw)
+        Ck = venom.spmm(x, Bt, b_kmajor=True, **kw)
+        assert torch.equal(Ck, C)
+        check_spmm(Ck, C_ref, dt)
+        Ckt = venom.spmm(x, Bt, b_kmajor=True, transposed_out=True, **kw)
+        assert torch.equal(Ckt.t(), C)
+
+
+def test_spmm_kmajor_b_on_2to4_form_is_torch_linear():
+    """The #18 V:2:4 form with K-major B and token-major C is F.linear on PyTorch-layout activations."""
+    R, K, T, V, M = 1024, 1024, 512, 64, 8
+    torch.manual_seed(3)
+    W = (torch.randn(R, K, device="cuda") * 0.02).half()
+    X = torch.randn(T, K, device="cuda").half()
+    x, y = venom.compress_2to4(W, V=V, M=M, check=True)
+    Y = venom.spmm(y, X, b_kmajor=True, transposed_out=True)
+    ref = torch.nn.functional.linear(X.float(), venom.decompress(x).float())
+    assert (Y.float() - ref).norm() / ref.norm() <= 2e-3
+    assert torch.equal(Y.t(), venom.spmm(y, X.t().contiguous()))
+    with pytest.raises(venom.VenomError):  # gathered (M != 4) operands take row-major B only
+        venom.spmm(x, X, b_kmajor=True)
