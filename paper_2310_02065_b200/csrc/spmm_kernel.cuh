@@ -295,18 +295,27 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
     if constexpr (kCT) {
-      // token-major C (C^T[t][r]): for each column t the warp's 32 lanes hold 32 consecutive rows,
-      // so one 16-bit store per lane writes 64 contiguous bytes of C^T row t — coalesced as is
-      if (row < p.R) {
+      // token-major C (C^T[t][r]): the warp's 32 lanes hold 32 consecutive rows of columns t, t+1
+      // (one packed word). Lane pairs swap halves with one shuffle so the even lane stores rows
+      // (r, r+1) of column t and the odd lane rows (r-1, r) of column t+1 as 32-bit words: every
+      // store instruction writes 64 contiguous bytes to each of two C^T rows
+      const bool odd = lane & 1;
+      const int64_t r0 = row - (odd ? 1 : 0);  // even row of the pair
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
+      for (int c = 0; c < NCH; ++c)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int64_t t = col_base + 32 * c + j;
-            if (32 * c + j < HC && t < p.T)
-              p.C[t * p.ldc + row] = static_cast<uint16_t>((pk[c][j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t w = pk[c][j];
+          const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+          const uint32_t v = odd ? ((o >> 16) | (w & 0xFFFF0000u)) : ((w & 0xFFFFu) | (o << 16));
+          const int jj = 32 * c + 2 * j + (odd ? 1 : 0);  // column within the warp's slice
+          const int64_t t = col_base + jj;
+          if (jj < HC && t < p.T && r0 < p.R) {
+            uint16_t* dst = p.C + t * p.ldc + r0;
+            if (r0 + 1 < p.R) *reinterpret_cast<uint32_t*>(dst) = v;
+            else *dst = static_cast<uint16_t>(v & 0xFFFFu);
           }
-      }
+        }
     } else if (p.dbg & 4) {  // ablation 4: no C stores
     } else if (stage_smem != 0 && !(p.dbg & 16384)) {  // ablation 16384: direct stores below
       // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
