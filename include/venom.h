@@ -228,6 +228,10 @@ typedef struct {
                         only (plain 2:4 or the V:2:4 form of venom_compress_2to4), one accumulator per
                         CTA (tile_t 240 and DENSE_K rejected). With c_transposed this is
                         Y = X·Wᵀ on [T, K] activations. 0: B row-major dtype[K][ldb] (default). */
+  int32_t activation;  /* 1: GELU (erf form, x·Φ(x)) applied after the bias in fp32 before the
+                        rounding; row-major B and C, gathered / contiguous kernel with one accumulator
+                        per CTA (else VENOM_ERR_INVALID_ARGUMENT). Not applied when K == 0.
+                        0: none (default). */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

@@ -52,7 +52,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
                 ("metadata_tc", ctypes.c_void_p), ("c_transposed", ctypes.c_int32),
-                ("b_kmajor", ctypes.c_int32)]
+                ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -279,13 +279,14 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
          max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0,
          use_metadata_tc: bool = True, transposed_out: bool = False,
-         b_kmajor: bool = False) -> torch.Tensor:
+         b_kmajor: bool = False, gelu: bool = False) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T], or with
     ``transposed_out`` the token-major C^T: dtype[T, R] (row stride may exceed R). When x carries
     tensor-core-ordered metadata (order_metadata) it is used unless use_metadata_tc is False.
     ``b_kmajor``: B is token-major dtype[T, K] (M = 4 operands); with ``transposed_out`` this is
-    ``F.linear(B, decompress(x))`` on PyTorch-layout activations."""
+    ``F.linear(B, decompress(x))`` on PyTorch-layout activations. ``gelu``: GELU after the bias in
+    the epilogue (row-major B and C)."""
     assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[1 if b_kmajor else 0] == x.K
     assert B.dtype == x.dtype
     T = B.shape[0 if b_kmajor else 1]
@@ -297,7 +298,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
     mtc = x.metadata_tc.data_ptr() if (use_metadata_tc and x.metadata_tc is not None) else None
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
-                 1 if b_kmajor else 0)
+                 1 if b_kmajor else 0, 1 if gelu else 0)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
                              ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
                              ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),

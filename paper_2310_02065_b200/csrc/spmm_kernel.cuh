@@ -49,6 +49,7 @@ struct SpmmParams {
   int b3d;  // M = 4: B map is 3-D [T/64][K][64] (one box per stage) instead of 2-D
   int c_t;  // C stored transposed (token-major): element (r, t) at C[t * ldc + r]
   int bk;   // B given K-major (token-major activations, dtype[T][ldb]); M = 4 operand only
+  int act;  // 1: GELU after the bias (row-major C only)
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -245,7 +246,11 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 // TMEM -> +bias (fp32) -> RNE to fp16/bf16 packed in registers; the accumulator buffer is released
 // to the MMA warp as soon as it has been read, and the 16-byte global stores overlap the next
 // tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
-template <class Cfg, bool kBF16, int CG = 1, bool kCT = false>
+// kGELU: GELU (erf form, torch.nn.functional.gelu) after the bias, in fp32 before the rounding —
+// a separate instantiation (a runtime activation branch slowed every SpMM)
+__device__ __forceinline__ float gelu_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
+
+template <class Cfg, bool kBF16, int CG = 1, bool kCT = false, bool kGELU = false>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane,
                                               uint32_t stage_smem = 0) {
@@ -285,7 +290,10 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        pk[c][j] = pack2<kBF16>(__uint_as_float(v[2 * j]) + bv, __uint_as_float(v[2 * j + 1]) + bv);
+        if constexpr (kGELU)
+          pk[c][j] = pack2<kBF16>(gelu_f(__uint_as_float(v[2 * j]) + bv), gelu_f(__uint_as_float(v[2 * j + 1]) + bv));
+        else
+          pk[c][j] = pack2<kBF16>(__uint_as_float(v[2 * j]) + bv, __uint_as_float(v[2 * j + 1]) + bv);
     }
     tc_fence_before();
     __syncwarp();
@@ -526,7 +534,7 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
   }
 }
 
-template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false>
+template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false, bool kGELU = false>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
-    else epilogue_role<Cfg, kBF16, CG, kCT>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
+    else epilogue_role<Cfg, kBF16, CG, kCT, kGELU>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high

@@ -113,6 +113,13 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUte
                                 : venom::vnm_spmm_kernel<Cfg, kBF16, false, true>)
                     : (p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, false>
                                 : venom::vnm_spmm_kernel<Cfg, kBF16, false, false>);
+  if constexpr (Cfg::MB == 1) {
+    // GELU epilogue (row-major C, row-major B; checked by the caller)
+    if (p.act) kern = p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, false, false, true>
+                               : venom::vnm_spmm_kernel<Cfg, kBF16, false, false, false, true>;
+  } else {
+    if (p.act) return VENOM_ERR_INVALID_ARGUMENT;
+  }
   if constexpr (Cfg::MB == 1 && Cfg::NB == 1 && Cfg::BNH % 64 == 0) {
     // K-major B (token-major activations): M = 4 operand only (checked by the caller)
     if (p.bk) kern = p.c_t ? venom::vnm_spmm_kernel<Cfg, kBF16, true, true, true>
@@ -546,6 +553,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     return VENOM_ERR_INVALID_ARGUMENT;
   if (bk && (f.m != 4 || strategy == VENOM_STRATEGY_DENSE_K || (opts && opts->tile_t == 240) || K % 8 != 0))
     return VENOM_ERR_INVALID_ARGUMENT;
+  const int act = opts ? opts->activation : 0;
+  if (act != 0 && (act != 1 || ct || bk || strategy == VENOM_STRATEGY_DENSE_K || !can_gather ||
+                   (opts && opts->tile_t == 240)))
+    return VENOM_ERR_INVALID_ARGUMENT;
   const bool has_tc = opts && opts->metadata_tc;
   // metadata is not read with pre-ordered metadata; column_idx is not read when M = 4 (identity)
   if (!C || (K > 0 && (!values || !B || (!metadata && !has_tc) || (!column_idx && f.m != 4))))
@@ -596,8 +607,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.is_bf16 = bf16;
   p.b3d = 0;
   p.bk = 0;
+  p.act = 0;
   p.c_t = ct ? 1 : 0;
   p.bk = bk ? 1 : 0;
+  p.act = act;
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -661,7 +674,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     // 512 × 240 pair tiles (two accumulators per CTA) land 1.45× fewer bytes per FLOP but expose a
     // larger last epilogue: measured better only with long k-loops and at least one full wave of
     // pair tiles
-    if (contiguous && pair == 2 && opts && opts->metadata_tc && !ct && !bk) {
+    if (contiguous && pair == 2 && opts && opts->metadata_tc && !ct && !bk && !act) {
       int sms = 148, dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -52,9 +52,9 @@ class SparseLinear:
         self.bias = bias
 
     def __call__(self, x_fm: torch.Tensor, out: Optional[torch.Tensor] = None,
-                 token_major: bool = False) -> torch.Tensor:
+                 token_major: bool = False, gelu: bool = False) -> torch.Tensor:
         assert x_fm.shape[0] == self.K, (x_fm.shape, self.K)
-        return spmm(self.op, x_fm, bias=self.bias, out=out, transposed_out=token_major)
+        return spmm(self.op, x_fm, bias=self.bias, out=out, transposed_out=token_major, gelu=gelu)
 
 
 @dataclass
@@ -164,8 +164,7 @@ class SparseEncoder:
         L["o"](self.attn_fm, out=self.o_tm, token_major=True)
         x1 = torch.empty_like(x)
         enc_add_layernorm(x, self.o_tm, L["ln1_w"], L["ln1_b"], cfg.eps, x1, self.x1_fm)
-        f1 = L["f1"](self.x1_fm, out=self.hid[:cfg.ffn])                      # [4h, T], FFN2's B
-        torch.ops.aten.gelu_(f1)                                               # in place
+        L["f1"](self.x1_fm, out=self.hid[:cfg.ffn], gelu=True)   # GELU in the epilogue; FFN2's B
         L["f2"](self.hid, out=self.f2_tm, token_major=True)
         out = torch.empty_like(x)
         enc_add_layernorm(x1, self.f2_tm, L["ln2_w"], L["ln2_b"], cfg.eps, out, self.x_fm)

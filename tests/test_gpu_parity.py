@@ -779,3 +779,22 @@ def test_spmm_kmajor_b_on_2to4_form_is_torch_linear():
     assert torch.equal(Y.t(), venom.spmm(y, X.t().contiguous()))
     with pytest.raises(venom.VenomError):  # gathered (M != 4) operands take row-major B only
         venom.spmm(x, X, b_kmajor=True)
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt", [(256, 1040, 264, 64, 10, F16), (512, 1024, 256, 128, 4, BF16),
+                                          (384, 1024, 200, 128, 16, F16)])
+def test_spmm_gelu_epilogue(R, K, T, V, M, dt):
+    """opts.activation = GELU: C = gelu(A·B + bias), gelu(v) = v·Φ(v) in fp32 before the output
+    rounding; against the oracle's fp64 product passed through the fp64 erf GELU."""
+    import math
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 300 + R + M, True)
+    C_lin = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    erf = np.vectorize(math.erf)
+    C_ref = 0.5 * C_lin * (1.0 + erf(C_lin / math.sqrt(2.0)))
+    x = vnm_from(parts, R, K, V, M, dt)
+    for pre in (False, True):
+        if pre:
+            venom.order_metadata(x)
+        check_spmm(venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), gelu=True), C_ref, dt)
+    with pytest.raises(venom.VenomError):
+        venom.spmm(x, to_dev(B, dt), gelu=True, transposed_out=True)
