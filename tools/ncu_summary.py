@@ -15,6 +15,17 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum"]
 
 
+def _hbm_peak() -> float:
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"])
+    except Exception:
+        return 6549.4
+
+
+HBM_PEAK = _hbm_peak()
+
+
 def full(rep, out, key=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -38,7 +49,7 @@ def full(rep, out, key=None):
         except Exception:
             pass
     # derived: achieved HBM GB/s against the measured peak, L2->SMEM feed, sparse tensor-pipe use
-    lines += ["", "| kernel | duration us | DRAM GB/s | % of HBM peak (6549.4 GB/s, MEASURED_PEAKS.json) | "
+    lines += ["", f"| kernel | duration us | DRAM GB/s | % of HBM peak ({HBM_PEAK} GB/s, MEASURED_PEAKS.json) | "
               "L2->SMEM GB/s | tensor pipe active % |", "|---|---|---|---|---|---|"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
              "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
@@ -51,7 +62,7 @@ def full(rep, out, key=None):
             xb = float(d["l1tex__m_xbar2l1tex_read_bytes.sum"]) * scale.get(uu["l1tex__m_xbar2l1tex_read_bytes.sum"], 1)
             tp = d.get("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active", "-")
             lines.append(f"| {d.get('Kernel Name', '?')[:60]} | {t * 1e6:.2f} | {db / t / 1e9:.0f} | "
-                         f"{db / t / 1e9 / 6549.4 * 100:.1f} | {xb / t / 1e9:.0f} | {tp} |")
+                         f"{db / t / 1e9 / HBM_PEAK * 100:.1f} | {xb / t / 1e9:.0f} | {tp} |")
         except Exception:
             pass
     open(out, "w").write("\n".join(lines) + "\n")
