@@ -798,3 +798,32 @@ def test_spmm_gelu_epilogue(R, K, T, V, M, dt):
         check_spmm(venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), gelu=True), C_ref, dt)
     with pytest.raises(venom.VenomError):
         venom.spmm(x, to_dev(B, dt), gelu=True, transposed_out=True)
+
+
+def test_tensor_parallel_allgather_on_gpu():
+    """paper_2310_02065_b200/tp.py over NCCL (a one-rank group on this GPU): token-major local SpMM +
+    all_gather_into_tensor gives C^T of the full product, bitwise venom.spmm's C transposed."""
+    import socket
+    import torch.distributed as dist
+    from paper_2310_02065_b200 import tp
+    R, K, T, V, M = 256, 512, 256, 128, 8
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, F16, 77, True)
+    x = vnm_from(parts, R, K, V, M, F16)
+    venom.order_metadata(x)
+    created = False
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0)
+        created = True
+    try:
+        Bd, bd = to_dev(B, F16), to_dev(bv, F16)
+        t0, t1 = tp.t_slice(T, dist.get_world_size(), dist.get_rank())
+        Ct = tp.spmm_tp_allgather(x, Bd[:, t0:t1], bias=bd)
+        torch.cuda.synchronize()
+        assert Ct.shape == (T, R)
+        assert torch.equal(Ct.t(), venom.spmm(x, Bd, bias=bd))
+    finally:
+        if created:
+            dist.destroy_process_group()

@@ -57,6 +57,19 @@ def _worker(rank: int, ws: int, port: int, q):
             C_cat = torch.cat(gathered, dim=1).numpy()
             assert np.array_equal(C_cat, C_full)
 
+        # tensor-parallel all-gather of C (paper_2310_02065_b200/tp.py): token-major slices gathered
+        # with one all_gather_into_tensor equal the unsharded product transposed (the local products
+        # stand in for the GPU SpMM with the oracle)
+        from paper_2310_02065_b200 import tp
+        t0, t1 = tp.t_slice(T, ws, rank)
+        assert (t0, t1) == (rank * ts, (rank + 1) * ts)
+        C_tm = torch.from_numpy(np.ascontiguousarray(C_r.T))          # [T/ws, R]
+        full_tm = tp.gather_token_major(C_tm)
+        if rank == 0:
+            assert np.array_equal(full_tm.numpy(), oracle.spmm(*parts, R, K, synth.F16, V, M, B).T)
+        with pytest.raises(ValueError):
+            tp.t_slice(100, ws, rank)
+
         # weak scaling draws per-rank activations: the ranks' B differ
         b_r = torch.from_numpy(synth.gaussian((8, 8), 1.0, synth.F16, 1001 + 7919 * rank).astype(np.int32))
         gb = [torch.empty_like(b_r) for _ in range(ws)]
