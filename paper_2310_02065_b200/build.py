@@ -10,12 +10,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libvenom.so")
-SOURCES = [os.path.join(HERE, "csrc", "venom_api.cu")]
+# venom_api.cu (C ABI, format kernels) plus the SpMM kernel instantiations split into units that
+# nvcc compiles in parallel (csrc/spmm_launch.cuh declares one launcher per unit)
+SOURCES = [os.path.join(HERE, "csrc", "venom_api.cu")] + sorted(glob.glob(os.path.join(HERE, "csrc", "tu_*.cu")))
 DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
     sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+LINK_FLAGS = [*ARCH, "-shared", "-cudart", "static"]
 
 
 def nvcc() -> str:
@@ -40,9 +43,20 @@ def build(force: bool = False, verbose: bool = False, ablation: bool = False) ->
     if not force and not needs_build(lib):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-DVENOM_ABLATION"] if ablation else []),
-           *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *SOURCES]
-    subprocess.check_call(cmd, cwd=HERE)
+    objdir = os.path.join(HERE, "build", "ablation" if ablation else "release")
+    os.makedirs(objdir, exist_ok=True)
+    extra = [*(["-DVENOM_ABLATION"] if ablation else []), *(["-Xptxas", "-v"] if verbose else [])]
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
+        objs.append(obj)
+        if os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(d) for d in DEPS) and not force:
+            continue
+        procs.append((src, subprocess.Popen([nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj, src], cwd=HERE)))
+    bad = [s for s, p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, f"nvcc {bad}")
+    subprocess.check_call([nvcc(), *LINK_FLAGS, "-o", tmp, *objs], cwd=HERE)
     os.replace(tmp, lib)
     return lib
 

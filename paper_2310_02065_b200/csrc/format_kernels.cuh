@@ -807,4 +807,13 @@ __global__ void vnm_energy_finish_kernel(double* out) {
   out[2] = (out[1] == 0.0) ? 1.0 : out[0] / out[1];
 }
 
+// C = bias (or 0) when K == 0 (no groups): nothing to multiply. transposed: C^T[t][r] layout.
+__global__ void vnm_fill_bias_kernel(uint16_t* C, int64_t R, int64_t T, int64_t ldc, const uint16_t* bias,
+                                     int transposed) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= R * T) return;
+  const int64_t r = idx / T, t = idx - r * T;
+  C[transposed ? t * ldc + r : r * ldc + t] = bias ? bias[r] : static_cast<uint16_t>(0);
+}
+
 }  // namespace venom

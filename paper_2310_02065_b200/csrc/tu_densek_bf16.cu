@@ -1,0 +1,9 @@
+// tu_densek_bf16.cu — dense-K SpMM kernel instantiations (one compilation unit of libvenom;
+// spmm_launch.cuh)
+#include "spmm_launch.cuh"
+
+namespace venom {
+namespace launch {
+venom_status_t densek_bf16(VENOM_DENSEK_ARGS) { return run_densek_cfg<true>(M, pair, tile_t, tb, enc, p, max_ctas, s); }
+}  // namespace launch
+}  // namespace venom

@@ -11,20 +11,14 @@
 #include "../../include/venom.h"
 #include "../../include/venom_encoder.h"
 #include "format_kernels.cuh"
-#include "densek_kernel.cuh"
-#include "spmm_kernel.cuh"
+#include "spmm_launch.cuh"
 #include "encoder_kernels.cuh"
 
 namespace {
 
-using venom::DenseKCfg;
-using venom::SpmmCfg;
 using venom::SpmmParams;
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using venom::launch::EncodeTiledFn;
+using venom::launch::launch_status;
 
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -73,178 +67,6 @@ int debug_flags() {
 #endif
 }
 
-venom_status_t launch_status() {
-  return cudaGetLastError() == cudaSuccess ? VENOM_OK : VENOM_ERR_CUDA;
-}
-
-// Launch with an optional CTA-pair cluster (cg = 2 -> cluster dims {2,1,1}).
-template <typename Kern, typename... Args>
-venom_status_t launch_cg(Kern kern, int cg, int grid, int threads, int smem, cudaStream_t s,
-                         Args... args) {
-  if (cg == 1) {
-    kern<<<grid, threads, smem, s>>>(args...);
-    return launch_status();
-  }
-  grid -= grid % cg;
-  if (grid < cg) grid = cg;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cg;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, args...) != cudaSuccess) return VENOM_ERR_CUDA;
-  return launch_status();
-}
-
-// ------------------------------------------------------------------ SpMM dispatch
-template <class Cfg, bool kBF16>
-venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUtensorMap& te,
-                        SpmmParams p, int max_ctas, cudaStream_t s) {
-  // token-major C is a separate instantiation: a runtime branch in the epilogue cost the row-major
-  // kernels up to 12% (measured on BERT FFN1)
-  auto kern = p.c_t ? (p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, true>
-                                : venom::vnm_spmm_kernel<Cfg, kBF16, false, true>)
-                    : (p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, false>
-                                : venom::vnm_spmm_kernel<Cfg, kBF16, false, false>);
-  if constexpr (Cfg::MB == 1) {
-    // GELU epilogue (row-major C, row-major B; checked by the caller)
-    if (p.act) kern = p.M == 4 ? venom::vnm_spmm_kernel<Cfg, kBF16, true, false, false, true>
-                               : venom::vnm_spmm_kernel<Cfg, kBF16, false, false, false, true>;
-  } else {
-    if (p.act) return VENOM_ERR_INVALID_ARGUMENT;
-  }
-  if constexpr (Cfg::MB == 1 && Cfg::NB == 1 && Cfg::BNH % 64 == 0) {
-    // K-major B (token-major activations): M = 4 operand only (checked by the caller)
-    if (p.bk) kern = p.c_t ? venom::vnm_spmm_kernel<Cfg, kBF16, true, true, true>
-                           : venom::vnm_spmm_kernel<Cfg, kBF16, true, false, true>;
-  } else {
-    if (p.bk) return VENOM_ERR_INVALID_ARGUMENT;
-  }
-  // >= 116 KB of shared memory guarantees one CTA per SM (each CTA allocates all 512 TMEM columns)
-  const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return VENOM_ERR_CUDA;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  p.m_tiles = static_cast<int>((p.R + 128 * Cfg::CG * Cfg::MB - 1) / (128 * Cfg::CG * Cfg::MB));
-  p.num_tiles = p.m_tiles * p.n_tiles;
-  int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (grid < 1) return VENOM_OK;
-  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, te, p);
-}
-
-template <class Cfg>
-venom_status_t run_spmm_dt(bool bf16, const CUtensorMap& tv, const CUtensorMap& tb,
-                           const CUtensorMap& te, SpmmParams p, int max_ctas, cudaStream_t s) {
-  return bf16 ? run_spmm<Cfg, true>(tv, tb, te, p, max_ctas, s)
-              : run_spmm<Cfg, false>(tv, tb, te, p, max_ctas, s);
-}
-
-// Gathered / contiguous kernel configurations. PRE: metadata pre-ordered for the tensor core.
-template <bool PRE>
-venom_status_t run_gather(int NBg, int pair, int tile_t, bool bf16, const CUtensorMap& tv,
-                          const CUtensorMap& tb, const CUtensorMap& te, SpmmParams p, int max_ctas,
-                          cudaStream_t s) {
-  using namespace venom;
-  if constexpr (PRE) {
-    // two 128-row blocks per CTA of a pair (512 × 240 pair tiles): 1.45× fewer landed bytes per
-    // useful FLOP than 256 × 256 pair tiles, for the contiguous (M = 4) operand
-    if (tile_t == 240 && NBg == 1 && pair == 2 && p.M == 4)
-      return run_spmm_dt<SpmmCfg<1, 240, 3, 4, 2, true, 2>>(bf16, tv, tb, te, p, max_ctas, s);
-  }
-  if (NBg == 1 && pair == 2) {
-    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 4, 8, 2, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 6, 8, 2, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-  } else if (NBg == 1) {
-    if (tile_t == 256) return run_spmm_dt<SpmmCfg<1, 256, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-    if (tile_t == 192) return run_spmm_dt<SpmmCfg<1, 192, 3, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<1, 128, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<1, 64, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-  } else if (NBg == 2) {
-    if (tile_t == 128) return run_spmm_dt<SpmmCfg<2, 128, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<2, 64, 4, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-  } else {
-    if (tile_t == 64) return run_spmm_dt<SpmmCfg<4, 64, 2, 8, 1, PRE>>(bf16, tv, tb, te, p, max_ctas, s);
-  }
-  return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
-}
-
-template <class Cfg, bool kBF16>
-venom_status_t run_densek(const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p, int max_ctas,
-                          cudaStream_t s) {
-  // compressed values: 2-D [R rows][2G] 16-bit, box VE × 128 rows (one k-stage), no swizzle
-  CUtensorMap tv;
-  {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * p.G), static_cast<cuuint64_t>(p.R)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(4 * static_cast<int64_t>(p.G))};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(Cfg::VE), 128};
-    cuuint32_t es[2] = {1, 1};
-    if (enc(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(p.values), dims, strides,
-            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return VENOM_ERR_CUDA;
-  }
-  auto kern = venom::vnm_spmm_densek_kernel<Cfg, kBF16>;
-  const int smem = Cfg::SMEM_BYTES < 116 * 1024 ? 116 * 1024 : Cfg::SMEM_BYTES;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return VENOM_ERR_CUDA;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (grid < 1) return VENOM_OK;
-  if constexpr (Cfg::CG == 1) {
-    kern<<<grid, Cfg::NUM_THREADS, smem, s>>>(tb, tv, p);
-  } else {
-    grid -= grid % Cfg::CG;  // whole CTA pairs
-    if (grid < Cfg::CG) grid = Cfg::CG;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(Cfg::NUM_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = Cfg::CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, tb, tv, p) != cudaSuccess) return VENOM_ERR_CUDA;
-  }
-  return launch_status();
-}
-
-template <int BN, int ST, int CG = 1>
-venom_status_t run_densek_m(int M, bool bf16, const CUtensorMap& tb, EncodeTiledFn enc, SpmmParams p,
-                            int max_ctas, cudaStream_t s) {
-  p.m_tiles = static_cast<int>((p.R + 128 * CG - 1) / (128 * CG));
-  p.num_tiles = p.m_tiles * p.n_tiles;
-#define VENOM_DK(MM)                                                                      \
-  case MM:                                                                                \
-    return bf16 ? run_densek<DenseKCfg<BN, ST, MM, CG>, true>(tb, enc, p, max_ctas, s)    \
-                : run_densek<DenseKCfg<BN, ST, MM, CG>, false>(tb, enc, p, max_ctas, s);
-  switch (M) {
-    VENOM_DK(4) VENOM_DK(8) VENOM_DK(16) VENOM_DK(32)
-  }
-#undef VENOM_DK
-  return VENOM_ERR_UNSUPPORTED_PATTERN;
-}
-
-// Cost model: both strategies are bound by max(tensor time, L2->SMEM
-// feed time) with the feed rates measured by tools/microbench.cu on B200 (gather of 128-byte rows
-// ~31 B/cycle/SM; 16 KB TMA boxes ~55 B/cycle/SM) and the sparse MMA issue rate (~13k dense-
-// equivalent FLOP/cycle/SM at N = 256). Returns relative costs in cycles·SM.
 }  // namespace
 
 extern "C" {
@@ -636,14 +458,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     if (tile_t == 0) tile_t = 256;
     set_tiles(tile_t);
     const int pair = opts && opts->cta_pair ? opts->cta_pair : 2;
-    if (pair == 2) {
-      if (tile_t == 256) return run_densek_m<256, 4, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
-      if (tile_t == 128) return run_densek_m<128, 6, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
-    } else {
-      if (tile_t == 256) return run_densek_m<256, 2>(f.m, bf16, tb, enc, p, max_ctas, s);
-      if (tile_t == 128) return run_densek_m<128, 4>(f.m, bf16, tb, enc, p, max_ctas, s);
-    }
-    return VENOM_ERR_INVALID_ARGUMENT;
+    return bf16 ? venom::launch::densek_bf16(f.m, pair, tile_t, tb, enc, p, max_ctas, s)
+                : venom::launch::densek_f16(f.m, pair, tile_t, tb, enc, p, max_ctas, s);
   }
 
   // gathered strategy
@@ -712,7 +528,9 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     return VENOM_ERR_CUDA;
   }
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
-  if (meta_tc == nullptr) return run_gather<false>(NBg, pair, tile_t, bf16, tv, tb, tv, p, max_ctas, s);
+  if (meta_tc == nullptr)
+    return bf16 ? venom::launch::gather_nopre_bf16(NBg, pair, tile_t, tv, tb, tv, p, max_ctas, s)
+                : venom::launch::gather_nopre_f16(NBg, pair, tile_t, tv, tb, tv, p, max_ctas, s);
   // pre-ordered metadata: the [tiles·num_ks] contiguous 2 KB stage blocks, mapped as 2-D
   // [blocks][256] u64 with a one-row box, so each block is one 2 KB TMA row (a 16-byte-wide box of
   // 128 rows would cost the TMA unit 128 row requests per stage)
@@ -729,7 +547,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return VENOM_ERR_CUDA;
   }
-  return run_gather<true>(NBg, pair, tile_t, bf16, tv, tb, te, p, max_ctas, s);
+  return bf16 ? venom::launch::gather_pre_bf16(NBg, pair, tile_t, tv, tb, te, p, max_ctas, s)
+              : venom::launch::gather_pre_f16(NBg, pair, tile_t, tv, tb, te, p, max_ctas, s);
 }
 
 int64_t venom_metadata_tc_bytes(int64_t R, int64_t K, venom_format_t f) {

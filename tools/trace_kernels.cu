@@ -9,6 +9,13 @@
 #include <vector>
 
 #include "../paper_2310_02065_b200/csrc/venom_api.cu"
+// the SpMM instantiation units of libvenom (one program here)
+#include "../paper_2310_02065_b200/csrc/tu_gather_pre_f16.cu"
+#include "../paper_2310_02065_b200/csrc/tu_gather_pre_bf16.cu"
+#include "../paper_2310_02065_b200/csrc/tu_gather_nopre_f16.cu"
+#include "../paper_2310_02065_b200/csrc/tu_gather_nopre_bf16.cu"
+#include "../paper_2310_02065_b200/csrc/tu_densek_f16.cu"
+#include "../paper_2310_02065_b200/csrc/tu_densek_bf16.cu"
 
 int main(int argc, char** argv) {
   const long R = argc > 1 ? atol(argv[1]) : 1024, K = argc > 2 ? atol(argv[2]) : 4096,
