@@ -134,7 +134,10 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  *   bias  nullable dtype[R], added in fp32 before rounding
  * Requirements (else VENOM_ERR_UNSUPPORTED_PATTERN / INVALID_ARGUMENT):
  *   V | R; M in [4,256], M | K; T % 8 == 0, ldb % 8 == 0, ldc % 8 == 0, ldb >= T, ldc >= T;
- *   values/B/C 16-byte aligned; and at least one strategy applies:
+ *   values/B/C 16-byte aligned, column_idx 4-byte aligned; metadata 16-byte aligned whenever it
+ *   is read (no opts->metadata_tc); dense-K additionally needs column_idx 16-byte aligned (a
+ *   misaligned view returns VENOM_ERR_INVALID_ARGUMENT instead of faulting on the device);
+ *   and at least one strategy applies:
  *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0
  *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
  *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
@@ -199,7 +202,8 @@ int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f);
  *   tile_t    output columns per CTA tile (64, 128, 192 or 256; availability depends on strategy;
  *             240 = 512 × 240 CTA-pair tiles with two accumulators per CTA, M == 4 operands with
  *             metadata_tc only. 0 = the planner's choice)
- *   stages    pipeline depth (where a variant exists)
+ *   stages    reserved: must be 0 (the pipeline depth is fixed per tile configuration; any other
+ *             value returns VENOM_ERR_INVALID_ARGUMENT)
  *   max_ctas  persistent grid cap (0 = #SMs)
  *   strategy  VENOM_STRATEGY_AUTO: the gathered/contiguous kernel wherever it applies, else
  *             DENSE_K; GATHER: the paper's mapping (gather the 4 selected
@@ -213,7 +217,8 @@ typedef struct {
   int32_t max_ctas;
   int32_t strategy;
   int32_t cta_pair;  /* 1 = one CTA per 128-row tile, 2 = CTA pair (cta_group::2, 256-row tiles,
-                        B split between the pair's shared memories); 0 = library default */
+                        B split between the pair's shared memories); 0 = library default; any
+                        other value returns VENOM_ERR_INVALID_ARGUMENT */
   const uint8_t* metadata_tc;  /* nullable DEVICE pointer: the operand's metadata in tensor-core
                         order (venom_order_metadata). When set, the gathered kernel loads it with
                         TMA and copies it to TMEM with tcgen05.cp instead of permuting `metadata`
@@ -232,6 +237,9 @@ typedef struct {
                         rounding; row-major B and C, gathered / contiguous kernel with one accumulator
                         per CTA (else VENOM_ERR_INVALID_ARGUMENT). Not applied when K == 0.
                         0: none (default). */
+  int32_t group_n;     /* tile order: column tiles are taken in groups of group_n, the row tiles
+                        outer within a group (1 = all row tiles of one column band first). 0: the
+                        library default (1). */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

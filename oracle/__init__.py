@@ -65,6 +65,7 @@ def _load():
         lib.oracle_spmm_compressed.argtypes = [P, P, P, I64, I64, I, I, I, I, P, I64, I64, P, P, I64]
         lib.oracle_gemm_dense.argtypes = [P, I64, I64, I64, I, P, I64, I64, P, P, I64]
         lib.oracle_num_threads.argtypes = []
+        lib.oracle_set_num_threads.argtypes = [I]
         lib.oracle_expand_2to4.argtypes = [P, P, P, I64, I64, I, I, I, P, P, P]
         lib.oracle_compress_masked.argtypes = [P, I64, I64, I64, I, P, I64, I, I, I, P, P, P]
         lib.oracle_energy.argtypes = [P, I64, I64, I64, I, P, I64, P]
@@ -92,6 +93,11 @@ def validate(R, K, V, N, M) -> int:
 
 def num_threads() -> int:
     return _load().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """Thread count of the OpenMP loops (timing legs only; n <= 0 = all host cores)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def compress(A: np.ndarray, dtype: int, V: int, M: int, N: int = 2, check: bool = True):

@@ -445,3 +445,15 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Thread-count control for the timing legs (bench.py cpu_baseline: single-thread and all-core
+ * runs); no arithmetic. n <= 0 restores the OpenMP default. */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  extern int omp_get_num_procs(void);
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+  (void)n;
+#endif
+}

@@ -52,7 +52,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
                 ("metadata_tc", ctypes.c_void_p), ("c_transposed", ctypes.c_int32),
-                ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32)]
+                ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32), ("group_n", ctypes.c_int32)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -181,6 +181,12 @@ def compress(A: torch.Tensor, V: int, M: int, N: int = 2, status: Optional[torch
     if check:
         s = int(status.item())
         _check(s, "venom_compress (device status)")
+    if out is not None:
+        if out.metadata_tc is not None:
+            # the tensor-core-ordered copy of the old metadata would pair stale m-indices with the
+            # new values in spmm: re-derive it from the new metadata (same stream, in order)
+            order_metadata(out, out=out.metadata_tc)
+        return out
     return VNMTensor(values, metadata, column_idx, R, K, V, M, N)
 
 
@@ -279,7 +285,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
          max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0,
          use_metadata_tc: bool = True, transposed_out: bool = False,
-         b_kmajor: bool = False, gelu: bool = False) -> torch.Tensor:
+         b_kmajor: bool = False, gelu: bool = False, group_n: int = 0) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T], or with
     ``transposed_out`` the token-major C^T: dtype[T, R] (row stride may exceed R). When x carries
@@ -298,7 +304,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
     mtc = x.metadata_tc.data_ptr() if (use_metadata_tc and x.metadata_tc is not None) else None
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
-                 1 if b_kmajor else 0, 1 if gelu else 0)
+                 1 if b_kmajor else 0, 1 if gelu else 0, group_n)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
                              ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
                              ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),

@@ -38,14 +38,17 @@ def needs_build(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, ablation: bool = False) -> str:
-    lib = ABLATION_LIB if ablation else LIB
+def build(force: bool = False, verbose: bool = False, ablation: bool = False, defines=(), name: str = "") -> str:
+    """`defines` / `name`: a tools-only variant (e.g. VENOM_GATHER_P=8 -> libvenom_<name>.so), never
+    the production library."""
+    lib = ABLATION_LIB if ablation else (os.path.join(HERE, f"libvenom_{name}.so") if name else LIB)
     if not force and not needs_build(lib):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
-    objdir = os.path.join(HERE, "build", "ablation" if ablation else "release")
+    objdir = os.path.join(HERE, "build", "ablation" if ablation else (name or "release"))
     os.makedirs(objdir, exist_ok=True)
-    extra = [*(["-DVENOM_ABLATION"] if ablation else []), *(["-Xptxas", "-v"] if verbose else [])]
+    extra = [*(["-DVENOM_ABLATION"] if ablation else []), *(["-Xptxas", "-v"] if verbose else []),
+             *[f"-D{d}" for d in defines]]
     objs, procs = [], []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
@@ -62,4 +65,7 @@ def build(force: bool = False, verbose: bool = False, ablation: bool = False) ->
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ablation="--ablation" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    names = [a[len("--name="):] for a in sys.argv[1:] if a.startswith("--name=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ablation="--ablation" in sys.argv,
+                defines=defs, name=names[0] if names else ""))

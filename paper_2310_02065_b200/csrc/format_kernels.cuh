@@ -609,7 +609,10 @@ __global__ void __launch_bounds__(256) vnm_expand_2to4_kernel(
       const uint32_t cw = __ldg(column_idx + rb * G + g);
       const uint32_t nib = (__ldg(metadata + row * meta_row + (g >> 1)) >> (4 * (g & 1))) & 0xFu;
       const uint32_t p0 = nib & 3u, p1 = nib >> 2;
-      bad |= !(p0 < p1) || ((cw >> 24) >= static_cast<uint32_t>(M));
+      // the same validity rule as vnm_decompress_kernel: m-indices ascending, column_idx strictly
+      // ascending and < M
+      bad |= !(p0 < p1) || !((cw & 0xFFu) < ((cw >> 8) & 0xFFu) && ((cw >> 8) & 0xFFu) < ((cw >> 16) & 0xFFu) &&
+                             ((cw >> 16) & 0xFFu) < (cw >> 24) && (cw >> 24) < static_cast<uint32_t>(M));
       const int c0 = static_cast<int>((cw >> (8 * p0)) & 0xFFu);
       const int c1 = static_cast<int>((cw >> (8 * p1)) & 0xFFu);
       const uint32_t v = __ldg(values + row * G + g);

@@ -45,6 +45,8 @@ struct SpmmParams {
   int m_tiles;   // ceil(R / 128)
   int n_tiles;   // ceil(T / BN)
   int num_tiles;
+  int group_n;   // tile order: groups of group_n column tiles, row tiles outer within a group
+                 // (L2 reuse of both A and B across the CTAs running at the same time; 1 = T-band order)
   int is_bf16;
   int b3d;  // M = 4: B map is 3-D [T/64][K][64] (one box per stage) instead of 2-D
   int c_t;  // C stored transposed (token-major): element (r, t) at C[t * ldc + r]
@@ -83,7 +85,7 @@ struct SpmmCfg {
   static constexpr int ACC_BUFS = (2 * ACC_COLS + E_PER_STAGE * STAGES_ <= 512) ? 2 : 1;
   static constexpr int E_COL = ACC_BUFS * ACC_COLS;
   static constexpr int NOPS = NB * NCH * 32;  // gather4 ops per stage (one per group × chunk × block)
-  static constexpr int OPS_PER_WARP = NOPS / P;
+  static constexpr int OPS_PER_WARP = (NOPS + P - 1) / P;  // the last warp may get fewer
   static constexpr int LANE_OPS = (OPS_PER_WARP + 31) / 32;
   // warp roles: [0,P) producers, P MMA, P+1..P+8 epilogue, P+9..P+12 metadata; epilogue and
   // metadata warps address TMEM lane quarter (warp % 4)
@@ -92,7 +94,6 @@ struct SpmmCfg {
   static constexpr int EPI_WARPS = (MB_ == 2) ? 16 : 8;
   static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 1 + EPI_WARPS;
   static constexpr int NUM_THREADS = 32 * (P + 1 + EPI_WARPS + (PRE_ ? 0 : 4));
-  static_assert(NOPS % P == 0, "gather ops must split evenly over producer warps");
   static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
   static constexpr int BAR_BYTES = 256;
   // per epilogue warp: one 32-row output chunk (64 B rows; 32 B rows for MB = 2)
@@ -145,14 +146,23 @@ __device__ __forceinline__ void load_meta_stage(const SpmmParams& p, int64_t row
   }
 }
 
-// Persistent static schedule: CTA b runs tiles b, b + grid, b + 2·grid, ... in T-band order (all
-// row tiles of one column band first, so concurrently running CTAs share the B column slab in L2).
-// With CTA pairs (CG = 2) the unit of scheduling is the cluster: pair b runs tiles b, b + pairs...
+// Persistent static schedule: CTA b runs tiles b, b + grid, b + 2·grid, ... With CTA pairs (CG = 2)
+// the unit of scheduling is the cluster: pair b runs tiles b, b + pairs, ...
+// Tile order: the column tiles are cut into groups of group_n; within a group the row tiles are
+// outer and the group's column tiles inner, so the grid's concurrently running tiles cover about
+// grid / group_n row tiles × group_n column tiles — each A row tile and each B column slab is then
+// streamed from HBM by several CTAs at once (group_n = 1, the default, is the T-band order: all row
+// tiles of one column band first; spmm_launch.cuh).
 template <int CG = 1>
 __device__ __forceinline__ void tile_coords(const SpmmParams& p, int tl, int& m_tile, int& n_tile) {
   const int t = static_cast<int>(blockIdx.x) / CG + tl * (static_cast<int>(gridDim.x) / CG);
-  n_tile = t / p.m_tiles;
-  m_tile = t - n_tile * p.m_tiles;
+  const int per_group = p.m_tiles * p.group_n;
+  const int grp = t / per_group;
+  const int rem = t - grp * per_group;
+  const int n0 = grp * p.group_n;
+  const int gw = min(p.group_n, p.n_tiles - n0);  // the last group may be narrower
+  m_tile = rem / gw;
+  n_tile = n0 + (rem - m_tile * gw);
 }
 template <int CG = 1>
 __device__ __forceinline__ int my_tile_count(const SpmmParams& p) {
@@ -589,7 +599,6 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   const int total = my_tiles * p.num_ks;  // k-stage iterations this CTA runs
   const int nrb = static_cast<int>(p.R / p.V);
   const int row_off = 128 * static_cast<int>(rank);
-  const bool contiguous = (p.M == 4);  // column_idx ≡ {0,1,2,3}: B' is a plain K-slice of B
 
   auto tile_of = [&](int tl, int& m_tile, int& n_tile) { tile_coords<CG>(p, tl, m_tile, n_tile); };
   auto block_of = [&](int m_tile, int b) -> int {
@@ -602,58 +611,75 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
       producer_contiguous<Cfg, kBK>(p, &tm_values, &tm_b, &tm_e, my_tiles, smem0, full0, empty0, rank, warp);
   } else if (warp < Cfg::P) {
     // ======================= producers: values tile + gathered B' rows =======================
-    // Stage ops are (block b, chunk c, group q); warp w issues ops [w·OPS_PER_WARP, ...), one per
-    // lane: TMA issue is serial within a warp, so the gathers are spread over P warps. With a CTA
-    // pair every TMA signals the leader's barrier (cta_group::2 forms).
+    // (M > 4; M = 4 runs producer_contiguous.) Stage ops are (block b, chunk c, group q); warp w
+    // issues ops [w·OPS_PER_WARP, ...), one per lane: TMA issue is serial within a warp, so the
+    // gathers are spread over P warps. A lane's op (b, c, q) is the same in every stage, and the
+    // tile / k-stage cursors advance incrementally (no per-stage divisions: the producer's own
+    // instruction count sets how fast it refills the ring). With a CTA pair every TMA signals the
+    // leader's barrier (cta_group::2 forms).
     const uint64_t pol_a = policy_evict_first();
     const uint64_t pol_b = policy_evict_last();
-    uint32_t cw[kPrefetch][Cfg::LANE_OPS];
-    auto op_of = [&](int j, int& b, int& c, int& q) -> bool {
-      const int o_local = lane + 32 * j;
-      if (o_local >= Cfg::OPS_PER_WARP) return false;
-      const int o = warp * Cfg::OPS_PER_WARP + o_local;
-      b = o / (Cfg::NCH * 32);
-      c = (o / 32) % Cfg::NCH;
-      q = o % 32;
-      return true;
-    };
-    auto fetch = [&](int it, uint32_t (&w)[Cfg::LANE_OPS]) {
-      if (it >= total || contiguous) return;
-      int m_tile, n_tile;
-      tile_of(it / p.num_ks, m_tile, n_tile);
+    int ob[Cfg::LANE_OPS], oc[Cfg::LANE_OPS], oq[Cfg::LANE_OPS];
+    bool olive[Cfg::LANE_OPS];
 #pragma unroll
-      for (int j = 0; j < Cfg::LANE_OPS; ++j) {
-        int b, c, q;
-        w[j] = 0u;
-        if (!op_of(j, b, c, q)) continue;
-        const int gg = (it % p.num_ks) * Cfg::KG + q;
-        if (gg < p.G)
-          w[j] = __ldg(reinterpret_cast<const uint32_t*>(p.column_idx) +
-                       static_cast<int64_t>(block_of(m_tile, b)) * p.G + gg);
+    for (int j = 0; j < Cfg::LANE_OPS; ++j) {
+      const int o_local = lane + 32 * j;
+      const int o = warp * Cfg::OPS_PER_WARP + o_local;
+      // the last warp's share is short when P does not divide NOPS
+      olive[j] = o_local < Cfg::OPS_PER_WARP && o < Cfg::NOPS;
+      ob[j] = olive[j] ? o / (Cfg::NCH * 32) : 0;
+      oc[j] = olive[j] ? (o / 32) % Cfg::NCH : 0;
+      oq[j] = olive[j] ? o % 32 : 0;
+    }
+    const uint32_t* cidx = reinterpret_cast<const uint32_t*>(p.column_idx);
+    // column_idx words of this lane's ops for the tile the prefetch cursor is in
+    auto tile_cptr = [&](int tl, const uint32_t* (&cp)[Cfg::LANE_OPS]) {
+      int m_tile, n_tile;
+      tile_of(tl, m_tile, n_tile);
+#pragma unroll
+      for (int j = 0; j < Cfg::LANE_OPS; ++j) cp[j] = cidx + static_cast<int64_t>(block_of(m_tile, ob[j])) * p.G + oq[j];
+    };
+    // prefetch cursor: kPrefetch k-stages ahead of the issue cursor (the paper's two-level
+    // pre-fetching of column-loc)
+    int ftl = 0, fks = 0;
+    const uint32_t* fcp[Cfg::LANE_OPS];
+    if (my_tiles > 0) tile_cptr(0, fcp);
+    auto fetch_next = [&](uint32_t (&w)[Cfg::LANE_OPS]) {
+      if (ftl >= my_tiles) return;
+#pragma unroll
+      for (int j = 0; j < Cfg::LANE_OPS; ++j)
+        w[j] = (olive[j] && fks * Cfg::KG + oq[j] < p.G) ? __ldg(fcp[j] + fks * Cfg::KG) : 0u;
+      if (++fks == p.num_ks) {
+        fks = 0;
+        if (++ftl < my_tiles) tile_cptr(ftl, fcp);
       }
     };
+    uint32_t cw[kPrefetch][Cfg::LANE_OPS];
 #pragma unroll
-    for (int j = 0; j < kPrefetch; ++j) fetch(j, cw[j]);
+    for (int j = 0; j < kPrefetch; ++j) fetch_next(cw[j]);
+    // issue cursor
+    int tl = 0, ks = 0, stage = 0;
+    uint32_t phase = 0;
+    int m_tile = 0, n_tile = 0, col0 = 0, arow = 0;
+    auto set_tile = [&]() {
+      tile_of(tl, m_tile, n_tile);
+      col0 = n_tile * BN + static_cast<int>(rank) * Cfg::BNH;
+      arow = m_tile * 128 * CG * Cfg::MB + row_off;
+    };
+    if (my_tiles > 0) set_tile();
+    // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load, 2048 no metadata load
+    const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES) +
+                              (p.dbg & 2048 ? 0 : Cfg::E_BYTES));
     for (int it0 = 0; it0 < total; it0 += kPrefetch) {
 #pragma unroll
       for (int jj = 0; jj < kPrefetch; ++jj) {
         const int it = it0 + jj;
         if (it < total) {
-          const int stage = it % STAGES;
-          const uint32_t phase = (it / STAGES) & 1;
-          int m_tile, n_tile;
-          tile_of(it / p.num_ks, m_tile, n_tile);
-          const int ks = it % p.num_ks;
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t sbase = smem0 + stage * Cfg::STAGE_BYTES;
           const uint32_t fbar = (CG == 2) ? mapa_shared(full0 + 8 * stage, 0) : full0 + 8 * stage;
-          const int col0 = n_tile * BN + static_cast<int>(rank) * Cfg::BNH;
-          const int arow = m_tile * 128 * CG * Cfg::MB + row_off;
           if (warp == 0 && lane == 0) {
             VENOM_TRACE_EVENT(0, it);
-            // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load
-            const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES) +
-                                      (p.dbg & 2048 ? 0 : Cfg::E_BYTES));  // 2048: no metadata load
             if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
             if (!(p.dbg & 16)) {
 #pragma unroll
@@ -675,48 +701,35 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
               }
             }
           }
-          if (contiguous && p.b3d && warp == 1 && lane == 0 && !(p.dbg & 1)) {
-            // M = 4: the 4 "selected" rows of every group are the group itself, so B' is a plain
-            // K-slice of B: one 3-D box [NCH chunks][128 rows][64 columns] per stage (every TMA op
-            // costs the issuing warp a fixed overhead, so fewer, larger ops land faster)
-            const uint32_t bdst = sbase + Cfg::A_BYTES;
-            if constexpr (CG == 2) tma_load_3d_2sm(bdst, &tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
-            else tma_load_3d(bdst, &tm_b, fbar, 0, ks * 128, col0 / 64, pol_b);
-          }
-          if (contiguous && !p.b3d && lane == 0 && !(p.dbg & 1)) {
-            // M = 4 with T % 64 != 0: 2-D boxes, one per 64-column chunk, on different warps
-#pragma unroll
-            for (int b = 0; b < NB; ++b)
-#pragma unroll
-              for (int c = 0; c < Cfg::NCH; ++c) {
-                if ((1 + b * Cfg::NCH + c) % Cfg::P != warp) continue;
-                const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK;
-                if constexpr (CG == 2) tma_load_2d_2sm(bdst, &tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
-                else tma_load_2d(bdst, &tm_b, fbar, col0 + 64 * c, ks * 128, pol_b);
-              }
-          }
-          if (!contiguous && !(p.dbg & 1)) {
+          if (!(p.dbg & 1)) {
 #pragma unroll
             for (int j = 0; j < Cfg::LANE_OPS; ++j) {
-              int b, c, q;
-              if (!op_of(j, b, c, q)) continue;
-              const int gg = ks * Cfg::KG + q;
+              if (!olive[j]) continue;
+              const int gg = ks * Cfg::KG + oq[j];
               const uint32_t w = cw[jj][j];
               int r[4];
 #pragma unroll
               for (int t = 0; t < 4; ++t)
                 r[t] = (gg < p.G) ? gg * p.M + static_cast<int>((w >> (8 * t)) & 0xFF)
                                   : static_cast<int>(p.K);  // past the last row: zero fill
-              const uint32_t bdst = sbase + Cfg::A_BYTES + b * Cfg::B_BYTES + c * Cfg::B_CHUNK + q * 512;
+              const uint32_t bdst = sbase + Cfg::A_BYTES + ob[j] * Cfg::B_BYTES + oc[j] * Cfg::B_CHUNK + oq[j] * 512;
               if constexpr (CG == 2)
-                tma_gather4_2sm(bdst, &tm_b, fbar, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
+                tma_gather4_2sm(bdst, &tm_b, fbar, col0 + 64 * oc[j], r[0], r[1], r[2], r[3], pol_b);
               else
-                tma_gather4(bdst, &tm_b, fbar, col0 + 64 * c, r[0], r[1], r[2], r[3], pol_b);
+                tma_gather4(bdst, &tm_b, fbar, col0 + 64 * oc[j], r[0], r[1], r[2], r[3], pol_b);
             }
           }
           __syncwarp();
           if (warp == 0 && lane == 0) VENOM_TRACE_EVENT(4, it);
-          fetch(it + kPrefetch, cw[jj]);
+          fetch_next(cw[jj]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++ks == p.num_ks) {
+            ks = 0;
+            if (++tl < my_tiles) set_tile();
+          }
         }
       }
     }

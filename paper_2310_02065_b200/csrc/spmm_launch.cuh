@@ -14,6 +14,10 @@
 #include "spmm_kernel.cuh"
 #include "densek_kernel.cuh"
 
+#ifndef VENOM_GATHER_P
+#define VENOM_GATHER_P 11  // gather-issuing warps of the single-CTA 128 × 256 tile (tools builds vary it)
+#endif
+
 namespace venom {
 namespace launch {
 
@@ -93,6 +97,11 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUte
   int grid = p.num_tiles * Cfg::CG < sms ? p.num_tiles * Cfg::CG : sms;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid < 1) return VENOM_OK;
+  // tile order (opts.group_n): the T-band order (1) is the default. Grouping column tiles so that A
+  // is re-read from HBM less often (group_n = 3 roughly halves the GPT-3 FFN layer's DRAM traffic)
+  // measured slower there (2.16 vs 2.01 ms): the gathers of B are the latency-critical stream, and
+  // the T-band order keeps the fewest B column slabs live in L2
+  if (p.group_n <= 0) p.group_n = 1;
   return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, te, p);
 }
 
@@ -110,7 +119,10 @@ venom_status_t run_gather(int NBg, int pair, int tile_t, const CUtensorMap& tv, 
     if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 4, 8, 2, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
     if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 6, 8, 2, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
   } else if (NBg == 1) {
-    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 2, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
+    // 11 gather-issuing warps: TMA instructions issue serially within a warp, and a stage's 128
+    // gather4 ops spread over 12-15 warps land ~1.1-1.15x faster than over 8
+    // (tools/microbench_feed.cu); 20 warps in all keep 96 registers per thread (21 would cap at 80)
+    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 2, VENOM_GATHER_P, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
     if (tile_t == 192) return run_spmm<SpmmCfg<1, 192, 3, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
     if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 4, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
     if (tile_t == 64) return run_spmm<SpmmCfg<1, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
@@ -155,6 +167,7 @@ venom_status_t run_densek_m(int M, const CUtensorMap& tb, EncodeTiledFn enc, Spm
                             cudaStream_t s) {
   p.m_tiles = static_cast<int>((p.R + 128 * CG - 1) / (128 * CG));
   p.num_tiles = p.m_tiles * p.n_tiles;
+  p.group_n = 1;
   switch (M) {
     case 4: return run_densek<DenseKCfg<BN, ST, 4, CG>, kBF16>(tb, enc, p, max_ctas, s);
     case 8: return run_densek<DenseKCfg<BN, ST, 8, CG>, kBF16>(tb, enc, p, max_ctas, s);

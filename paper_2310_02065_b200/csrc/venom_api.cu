@@ -359,8 +359,14 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   const int V = f.v;
   const int64_t G = K / f.m;
   const bool can_gather = (f.m == 4 || V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0);
-  const bool can_densek = (f.m % 4 == 0) && (f.m <= 32) && (G % 4 == 0);
+  // dense-K is instantiated for M in {4, 8, 16, 32} only (spmm_launch.cuh run_densek_m)
+  const bool can_densek = (f.m == 4 || f.m == 8 || f.m == 16 || f.m == 32) && (G % 4 == 0);
   const int strategy = opts ? opts->strategy : VENOM_STRATEGY_AUTO;
+  // cta_pair sizes the B tensor-map boxes: a value outside {0, 1, 2} would make the TMA deliver
+  // fewer bytes than the stage barrier expects (a hang), so it is refused before anything runs
+  if (opts && (opts->cta_pair < 0 || opts->cta_pair > 2)) return VENOM_ERR_INVALID_ARGUMENT;
+  // the pipeline depth is fixed per tile configuration (spmm_launch.cuh); no override exists
+  if (opts && opts->stages != 0) return VENOM_ERR_INVALID_ARGUMENT;
   if (strategy == VENOM_STRATEGY_GATHER && !can_gather) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (strategy == VENOM_STRATEGY_DENSE_K && !can_densek) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (strategy < 0 || strategy > 2) return VENOM_ERR_INVALID_ARGUMENT;
@@ -385,6 +391,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     return VENOM_ERR_INVALID_ARGUMENT;
   if (!aligned(C, 16) || (K > 0 && (!aligned(values, 16) || !aligned(B, 16) || !aligned(column_idx, 4))))
     return VENOM_ERR_INVALID_ARGUMENT;
+  // canonical metadata is read with 16-byte vector loads (gathered kernel without metadata_tc, and
+  // the dense-K expanders), column_idx with 16-byte loads by the dense-K expanders: a misaligned
+  // view would fault on the device, so it is refused here
+  if (K > 0 && !has_tc && !aligned(metadata, 16)) return VENOM_ERR_INVALID_ARGUMENT;
   if (K > 0x7FFFFFFF || T > 0x7FFFFFFF || R > 0x7FFFFFFF) return VENOM_ERR_INVALID_ARGUMENT;
   if ((st = check_arch()) != VENOM_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -401,7 +411,6 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (!enc) return VENOM_ERR_CUDA;
   const int NB = (V % 128 == 0) ? 1 : 128 / V;
   const int max_ctas = opts ? opts->max_ctas : 0;
-  const int stages = opts ? opts->stages : 0;
   int tile_t = opts ? opts->tile_t : 0;
 
   bool use_densek;
@@ -426,6 +435,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.G = static_cast<int>(G);
   p.meta_row = static_cast<int>((G + 1) / 2);
   p.m_tiles = static_cast<int>((R + 127) / 128);
+  p.group_n = opts ? opts->group_n : 0;  // 0: the planner's tile order (spmm_launch.cuh)
   p.is_bf16 = bf16;
   p.b3d = 0;
   p.bk = 0;
@@ -449,7 +459,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
 
-  if (use_densek && (!metadata || !column_idx)) return VENOM_ERR_INVALID_ARGUMENT;
+  if (use_densek && (!metadata || !column_idx || !aligned(metadata, 16) || !aligned(column_idx, 16)))
+    return VENOM_ERR_INVALID_ARGUMENT;
   if (use_densek) {
     // B: 2-D [K rows][T], box 64 columns × 128 rows (one K-stage of one 64-column chunk), SW128
     CUtensorMap tb;
@@ -499,7 +510,6 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     }
   }
   set_tiles(tile_t);
-  (void)stages;
   p.b3d = contiguous && !bk && (T % 64 == 0) && ((tile_t / pair) % 64 == 0);
   if (p.b3d) {
     const int nch = (tile_t / pair + 63) / 64;
