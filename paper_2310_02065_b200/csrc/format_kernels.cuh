@@ -6,9 +6,12 @@
 // ascending rows; #3 two-stage greedy; #5/#6 ties -> lower index; #7 ascending storage; #8 nibble
 // packing) are what make the output byte-identical to the CPU oracle.
 #pragma once
+#include <cuda.h>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include "ptx_sm100.cuh"
 
 namespace venom {
 
@@ -208,172 +211,303 @@ __global__ void __launch_bounds__(256) vnm_compress_kernel(
   }
 }
 
-// Compression, shared-memory tile variant (the default when V·W·2 bytes fit): the CTA's V × W
-// block of A (W = gpc·M columns) is read from HBM exactly once with 16-byte loads, all in flight
-// together, then the three phases of vnm_compress_kernel run on the shared-memory copy:
-//   phase 1: thread per column, fp64 sum of |a| over the V rows in ascending order (the oracle's
-//            order; exact for fp16, so bit-identical scores — DESIGN.md reading #2);
-//   phase 2: thread per group: top-4 columns by (score desc, index asc), stored ascending;
-//   phase 3: thread per (row, pair of groups): top-2 of the 4 by (|a| desc, position asc), raw-bit
-//            value copy, nibble packing.
+// Shared-memory layout of vnm_compress_tile_kernel (host and device agree on it): the V × W tile
+// (16-bit), NS row-slice partial column sums (fp32), the column scores (fp64), per group the
+// selected-column word, the 4th / 5th largest score and a flag, a per-column "selected" byte, and
+// with kExpand the re-encoding's nibbles [V][W/8].
+struct CompressTileLayout {
+  static constexpr int NS = 8;  // row slices of the approximate column sums
+  size_t tile, tile_bytes, part, score, sel, th, rank, m2, total;
+  // swz: the tile as ceil(W / 64) boxes of V rows × 128 B with the 128-byte TMA swizzle (each box
+  // 1 KB aligned); else rows of W + 8 elements (a 16-byte pad per row). Either way the 8 rows a
+  // column-wise access touches fall in 8 different bank groups (a dense 256-byte pitch put them
+  // all in the same banks: 8-way conflicts in phase 3).
+  __host__ __device__ CompressTileLayout(int V, int W, int gpc, bool expand, int ntiles = 1, bool swz = false) {
+    tile = 0;
+    tile_bytes = swz ? static_cast<size_t>((W + 63) / 64) * ((static_cast<size_t>(V) * 128 + 1023) & ~size_t(1023))
+                     : ((static_cast<size_t>(V) * (W + 8) * 2 + 1023) & ~size_t(1023));
+    part = tile_bytes * ntiles;
+    score = part + static_cast<size_t>(NS) * W * 4;
+    sel = score + static_cast<size_t>(W) * 8;
+    th = sel + ((static_cast<size_t>(gpc) * 4 + 15) & ~size_t(15));
+    rank = th + static_cast<size_t>(gpc) * 16;
+    m2 = rank + ((static_cast<size_t>(W) + 15) & ~size_t(15));
+    total = m2 + (expand ? static_cast<size_t>(V) * (W / 8) : 0) + 16 + 1024;  // + 1 KB base alignment
+  }
+};
+
+// Element addressing of a compressor tile in shared memory (see CompressTileLayout).
+struct TileView {
+  const uint16_t* base;
+  int pitch;      // padded: row pitch in elements (W + 8)
+  int box;        // swizzled: elements per 64-column box (V·64 rounded to 1 KB)
+  bool swz;
+  __device__ __forceinline__ int idx(int i, int c) const {
+    return swz ? (c >> 6) * box + i * 64 + (((((c >> 3) & 7) ^ (i & 7))) << 3) + (c & 7) : i * pitch + c;
+  }
+  __device__ __forceinline__ uint16_t at(int i, int c) const { return base[idx(i, c)]; }
+  // the 8 columns 8·cv .. 8·cv + 7 of row i (16-byte aligned)
+  __device__ __forceinline__ uint4 vec(int i, int cv) const {
+    return *reinterpret_cast<const uint4*>(base + idx(i, 8 * cv));
+  }
+};
+
+// Compression, shared-memory tile variant (the default when the V × W tile fits): the CTA's V × W
+// block of A (W = gpc·M columns) is read from HBM once with 16-byte loads, all in flight together,
+// then:
+//   phase 1: column L1 mass. The oracle's score is the fp64 sum of |a| over the V rows in ascending
+//            order (reading #2). Computing that for every column costs ~13 instructions per element
+//            (the compressor was instruction-bound at 1.2 TB/s), so the kernel first sums in fp32
+//            (|a| of fp16 / bf16 is exact in fp32; NS row slices, then the slices in order) and
+//            only decides from those where they cannot be wrong: an fp32 sum of n non-negative terms
+//            is within n·2^-24 (relative) of the exact sum, so when the 4th and 5th largest
+//            approximate scores of a group differ by more than twice that bound, the exact top-4
+//            set — which is all the format stores (reading #7: ascending) — is the approximate one.
+//            Groups that fail the margin test (near-ties, all-zero blocks, fp32 overflow) get the
+//            exact scores: fp16 as integer sums of |a| in units of 2^-24 (exact, so equal to the
+//            oracle's fp64 sum in any order), bf16 as the oracle's sequential fp64 sum.
+//   phase 2: rank of each column in its group by (score desc, index asc); rank < 4 is selected.
+//   phase 3: thread per (row, group): top-2 of the 4 by (|a| desc, position asc), raw-bit value
+//            copy, nibble packing (+ the V:2:4 re-encoding with kExpand).
+// Phases 1-4 of the compressor on one V × W tile already in shared memory (`tile`, pitch W); the
+// scratch arrays live at `smem_raw` + CompressTileLayout offsets. Called by the tile kernel (after
+// its own loads) and by the persistent TMA kernel (once per tile of its pipeline).
 template <bool kBF16, bool kExpand>
-__global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
-    const uint16_t* __restrict__ A, int64_t R, int64_t K, int64_t lda, int V, int M, int64_t G,
-    int gpc, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
-    uint8_t* __restrict__ column_idx, int32_t* __restrict__ status,
-    uint32_t* __restrict__ values2, uint32_t* __restrict__ meta_tc, int dbg) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int64_t rb = blockIdx.y;
-  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * gpc;
+__device__ __forceinline__ void compress_tile_process(
+    const TileView tile, uint8_t* smem_raw, int64_t R, int64_t K, int V, int M, int64_t G,
+    int gpc, int64_t rb, int64_t g0, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
+    uint8_t* __restrict__ column_idx, int32_t* __restrict__ status, uint32_t* __restrict__ values2,
+    uint32_t* __restrict__ meta_tc, int dbg, int nbuf) {
   const int ng = static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
   const int W = gpc * M;                 // tile pitch (elements)
   const int ncols = ng * M;
-  const int64_t k0 = g0 * M;
   const int64_t row0 = rb * V;
   const int64_t meta_row = (G + 1) / 2;
-  uint16_t* tile = reinterpret_cast<uint16_t*>(smem_raw);                        // [V][W]
-  double* s_score = reinterpret_cast<double*>(smem_raw + ((static_cast<size_t>(V) * W * 2 + 15) & ~size_t(15)));
-  uint32_t* s_sel = reinterpret_cast<uint32_t*>(s_score + W);                    // [gpc]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  constexpr int NS = CompressTileLayout::NS;
+  const CompressTileLayout lay(V, W, gpc, kExpand, nbuf, tile.swz);  // scratch after the nbuf tile buffers
+  float* s_part = reinterpret_cast<float*>(smem_raw + lay.part);       // [NS][W]
+  double* s_score = reinterpret_cast<double*>(smem_raw + lay.score);   // [W]
+  uint32_t* s_sel = reinterpret_cast<uint32_t*>(smem_raw + lay.sel);   // [gpc]
+  double* s_th = reinterpret_cast<double*>(smem_raw + lay.th);         // [gpc][2]: 4th, 5th score
+  uint8_t* s_rank = smem_raw + lay.rank;                               // [W]: selected?
   // kExpand: the V:2:4 re-encoding's nibbles of this tile, [V][W/8] bytes (subgroups 2j, 2j+1)
-  uint8_t* s_m2 = reinterpret_cast<uint8_t*>(s_sel + gpc);
+  uint8_t* s_m2 = smem_raw + lay.m2;
+  (void)K;
 
-  // ---- phase 0: the block tile, 16-byte loads (8 columns) where aligned, else element-wise
-  bool bad = false;
-  const int nvec = ncols / 8;  // full 8-column vectors of a row (W % 8 == 0 by construction)
-  const bool vec_ok = ((lda & 7) == 0) && ((k0 & 7) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  if (vec_ok && !(dbg & 1)) {
-    // 4 independent 16-byte loads in flight per thread before any of them is consumed
-    constexpr int U = 4;
-    const int nv = V * nvec;
-    for (int t0 = threadIdx.x; t0 < nv; t0 += U * blockDim.x) {
-      uint4 w[U];
+  // ---- phase 1a: approximate column sums: thread per (8-column vector, row slice), fp32
+  const int nv8 = (ncols + 7) / 8;
+  const int ns = (nthr / nv8) < NS ? ((nthr / nv8) > 0 ? nthr / nv8 : 1) : NS;
+  for (int t = tid; t < nv8 * ns; t += nthr) {
+    const int cv = t % nv8, sl = t / nv8;
+    const int r0 = (sl * V) / ns, r1 = ((sl + 1) * V) / ns;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (!(dbg & 2))
+      for (int i = r0; i < r1; ++i) {
+        const uint4 w = tile.vec(i, cv);
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u * static_cast<int>(blockDim.x);
-        if (t < nv) {
-          const int i = t / nvec, cv = t - i * nvec;
-          w[u] = __ldg(reinterpret_cast<const uint4*>(A + (row0 + i) * lda + k0) + cv);
+        for (int h = 0; h < 4; ++h) {
+          a[2 * h] += fabsf(bits_to_float<kBF16>(static_cast<uint16_t>(ww[h] & 0xFFFFu)));
+          a[2 * h + 1] += fabsf(bits_to_float<kBF16>(static_cast<uint16_t>(ww[h] >> 16)));
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u * static_cast<int>(blockDim.x);
-        if (t < nv) {
-          const int i = t / nvec, cv = t - i * nvec;
-          *reinterpret_cast<uint4*>(tile + i * W + 8 * cv) = w[u];
-          const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            bad |= bits_non_finite<kBF16>(static_cast<uint16_t>((ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu));
-        }
-      }
-    }
+    for (int e = 0; e < 8; ++e) s_part[sl * W + 8 * cv + e] = a[e];
   }
-  const int cstart = vec_ok ? 8 * nvec : 0;
-  const int ntail = ncols - cstart;
-  if (ntail > 0) {
-    for (int t = threadIdx.x; t < V * ntail; t += blockDim.x) {
-      const int i = t / ntail, c = cstart + (t - i * ntail);
-      const uint16_t b = __ldg(A + (row0 + i) * lda + k0 + c);
-      tile[i * W + c] = b;
-      bad |= bits_non_finite<kBF16>(b);
+  __syncthreads();
+  bool bad = false;
+  for (int c = tid; c < ncols; c += nthr) {
+    float sum = s_part[c];
+    for (int sl = 1; sl < ns; ++sl) sum += s_part[sl * W + c];
+    s_score[c] = static_cast<double>(sum);
+    if (!isfinite(sum)) {
+      // an inf / nan input makes the sum non-finite; bf16 sums of finite values can also overflow
+      // fp32, so the column itself is checked
+      if constexpr (kBF16) {
+        for (int i = 0; i < V; ++i) bad |= bits_non_finite<true>(tile.at(i, c));
+      } else {
+        bad = true;  // fp16: |a| <= 65504, so a finite column sums to < 2^40 (finite)
+      }
     }
   }
   if (bad && status != nullptr) atomicMax(status, kStatusNonFinite);
   __syncthreads();
 
-  // ---- phase 1: column L1 mass
-  if constexpr (!kBF16) {
-    // fp16: every |a| is k·2^-24 with integer k < 2^40 and the column sums stay < 2^53, so fp64
-    // addition is exact in any order — the oracle's sequential sum bit for bit (reading #2). Two
-    // threads per column (row halves, 4 independent chains each); the halves meet in shared memory.
-    double* s_half = reinterpret_cast<double*>(s_m2 + (kExpand ? V * (W / 8) : 0));
-    s_half = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_half) + 15) & ~uintptr_t(15));
-    for (int t = threadIdx.x; t < 2 * ncols; t += blockDim.x) {
-      const int c = t % ncols, hf = t / ncols;
-      const int r0 = hf * (V / 2), r1 = hf ? V : V / 2;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (!(dbg & 2)) {
-        int i = r0;
-        for (; i + 4 <= r1; i += 4) {
-          a0 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 0) * W + c])));
-          a1 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 1) * W + c])));
-          a2 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 2) * W + c])));
-          a3 += static_cast<double>(fabsf(bits_to_float<false>(tile[(i + 3) * W + c])));
-        }
-        for (; i < r1; ++i) a0 += static_cast<double>(fabsf(bits_to_float<false>(tile[i * W + c])));
+  // ---- phase 2a: rank of column j in its group by (score desc, index asc) = its place in the
+  // order the format selects by (reading #5); the 4th and 5th scores of each group are kept
+  auto rank_pass = [&](bool only_flagged) {
+    for (int t = tid; t < ncols; t += nthr) {
+      const int q = t / M, j = t - q * M;
+      if (only_flagged && s_th[2 * q + 1] >= 0.0) continue;  // exact pass: flagged groups only
+      const double* sc = s_score + q * M;
+      const double sj = sc[j];
+      int rank = 0;
+      for (int i = 0; i < M; ++i) rank += (sc[i] > sj) || (sc[i] == sj && i < j);
+      s_rank[t] = static_cast<uint8_t>(rank < 4 ? 1 : 0);
+      if (!only_flagged) {
+        if (rank == 3) s_th[2 * q] = sj;
+        if (rank == 4) s_th[2 * q + 1] = sj;
       }
-      s_half[hf * W + c] = (a0 + a1) + (a2 + a3);
     }
-    __syncthreads();
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) s_score[c] = s_half[c] + s_half[W + c];
-  } else {
-    // bf16: not exact in general — the oracle's order (ascending rows, fp64), one thread per column
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-      double acc = 0.0;
-      if (!(dbg & 2))
-        for (int i = 0; i < V; ++i) acc = __dadd_rn(acc, static_cast<double>(fabsf(bits_to_float<true>(tile[i * W + c]))));
-      s_score[c] = acc;
+  };
+  rank_pass(false);
+  __syncthreads();
+  // ---- phase 1b: the margin test, and exact scores for the groups that fail it
+  const double tol = 2.1 * static_cast<double>(V + NS) * 0x1p-24;
+  for (int q = tid; q < ng; q += nthr) {
+    bool ok = true;
+    if (M > 4) {
+      const double s4 = s_th[2 * q], s5 = s_th[2 * q + 1];
+      ok = (s4 - s5) > tol * s4 && s4 < 1e30;  // false for NaN / overflow (inf - inf)
     }
+    s_th[2 * q + 1] = ok ? 1.0 : -1.0;  // flag: >= 0 decided, < 0 exact pass
   }
   __syncthreads();
-
-  // ---- phase 2: the four most significant columns of each block
-  for (int q = threadIdx.x; q < ng; q += blockDim.x) {
-    const double* sc = s_score + q * M;
-    int c[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      int best = -1;
-      double bs = 0.0;
-      for (int j = 0; j < M; ++j) {
-        bool taken = false;
-#pragma unroll
-        for (int u = 0; u < t; ++u) taken |= (c[u] == j);
-        if (taken) continue;
-        if (best < 0 || sc[j] > bs) {
-          best = j;
-          bs = sc[j];
-        }
+  bool any_exact = false;
+  for (int t = tid; t < ncols; t += nthr) {
+    const int q = t / M;
+    if (s_th[2 * q + 1] >= 0.0) continue;
+    any_exact = true;
+    if constexpr (!kBF16) {
+      // fp16: every |a| is k·2^-24 with an integer k < 2^40 (k = m for subnormals, (1024 + m) <<
+      // (e - 1) for normals) and a column's sum stays < 2^53, so the oracle's fp64 sum is exact and
+      // equals the integer sum in any order; compared in units of 2^-24 (one scale per group)
+      uint64_t acc = 0;
+      for (int i = 0; i < V; ++i) {
+        const uint32_t hb = tile.at(i, t) & 0x7FFFu;
+        const uint32_t e = hb >> 10, m = hb & 0x3FFu;
+        acc += e ? (static_cast<uint64_t>(0x400u | m) << (e - 1)) : static_cast<uint64_t>(m);
       }
-      c[t] = best;
+      s_score[t] = static_cast<double>(acc);
+    } else {
+      // bf16: the oracle's order (ascending rows, fp64)
+      double acc = 0.0;
+      for (int i = 0; i < V; ++i) acc = __dadd_rn(acc, static_cast<double>(fabsf(bits_to_float<true>(tile.at(i, t)))));
+      s_score[t] = acc;
     }
-#define VENOM_CSWAP(x, y) \
-  if (c[x] > c[y]) {      \
-    int t_ = c[x];        \
-    c[x] = c[y];          \
-    c[y] = t_;            \
   }
-    VENOM_CSWAP(0, 1) VENOM_CSWAP(2, 3) VENOM_CSWAP(0, 2) VENOM_CSWAP(1, 3) VENOM_CSWAP(1, 2)
-#undef VENOM_CSWAP
-    const uint32_t word = static_cast<uint32_t>(c[0]) | (static_cast<uint32_t>(c[1]) << 8) |
-                          (static_cast<uint32_t>(c[2]) << 16) | (static_cast<uint32_t>(c[3]) << 24);
+  if (__syncthreads_or(any_exact)) {
+    rank_pass(true);
+    __syncthreads();
+  }
+  // ---- phase 2b: the four selected columns of each group, ascending (reading #7)
+  for (int q = tid; q < ng; q += nthr) {
+    uint32_t word = 0;
+    int n = 0;
+    for (int j = 0; j < M && n < 4; ++j)
+      if (s_rank[q * M + j]) word |= static_cast<uint32_t>(j) << (8 * n++);
     reinterpret_cast<uint32_t*>(column_idx)[rb * G + g0 + q] = word;
     s_sel[q] = word;
   }
   __syncthreads();
 
+  // ---- phase 3 (plain compression): thread per (pair of groups, row) — the pair fills one
+  // metadata byte and 8 value bytes; a thread keeps its pair's 8 selected column offsets in
+  // registers and steps over rows (pointer increments only)
+  if constexpr (!kExpand) {
+    const int npr = (ng + 1) / 2;  // group pairs per row
+    if (!(dbg & 4) && nthr % npr == 0) {
+      const int pp = tid % npr, rs = nthr / npr;
+      const int qa = 2 * pp, qb = 2 * pp + 1;
+      const bool has_b = qb < ng;
+      const uint32_t wa = s_sel[qa], wb = has_b ? s_sel[qb] : 0x03020100u;
+      int ca[4], cb[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        ca[t] = qa * M + static_cast<int>((wa >> (8 * t)) & 0xFFu);
+        cb[t] = qb * M + static_cast<int>((wb >> (8 * t)) & 0xFFu);
+      }
+      auto top2 = [](const uint16_t (&v)[4], uint32_t& word, uint32_t& nib) {
+        // top-2 by (|a| desc, position asc): keys (|a| << 2) | (3 - t) are distinct and order the
+        // candidates exactly so (|w| order for finite sign-magnitude values; ±0 tie); the two
+        // largest of four keys with six min/max operations, no branches
+        uint32_t k[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) k[t] = ((v[t] & 0x7FFFu) << 2) | static_cast<uint32_t>(3 - t);
+        const uint32_t a = max(k[0], k[1]), b = min(k[0], k[1]), c = max(k[2], k[3]), d = min(k[2], k[3]);
+        const uint32_t first = max(a, c), second = max(min(a, c), max(b, d));
+        const uint32_t pa = 3u - (first & 3u), pb = 3u - (second & 3u);
+        const uint32_t lo = min(pa, pb), hi = max(pa, pb);
+        const uint64_t vv = static_cast<uint64_t>(v[0]) | (static_cast<uint64_t>(v[1]) << 16) |
+                            (static_cast<uint64_t>(v[2]) << 32) | (static_cast<uint64_t>(v[3]) << 48);
+        word = static_cast<uint32_t>((vv >> (16 * lo)) & 0xFFFFu) | (static_cast<uint32_t>((vv >> (16 * hi)) & 0xFFFFu) << 16);
+        nib = lo | (hi << 2);
+      };
+      const int i0 = tid / npr;
+      uint32_t* vrow = reinterpret_cast<uint32_t*>(values) + (row0 + i0) * G + g0 + qa;
+      uint8_t* mrow = metadata + (row0 + i0) * meta_row + (g0 + qa) / 2;
+      const int64_t vstep = static_cast<int64_t>(rs) * G, mstep = static_cast<int64_t>(rs) * meta_row;
+      // the 8 selected columns' element offsets for row i0; a row step of rs moves every one of them
+      // by the same amount when the swizzle pattern (row % 8) repeats (rs % 8 == 0)
+      const bool inc = !tile.swz || (rs & 7) == 0;
+      int oa[4], ob[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        oa[t] = tile.idx(i0, ca[t]);
+        ob[t] = tile.idx(i0, cb[t]);
+      }
+      const int ostep = tile.swz ? rs * 64 : rs * tile.pitch;
+      const uint16_t* tb = tile.base;
+      // an odd G makes (row·G + g) odd on alternate rows: 8-byte stores only when aligned
+      for (int i = i0; i < V; i += rs, vrow += vstep, mrow += mstep, tb += ostep) {
+        uint16_t va[4], vb[4];
+        if (inc) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            va[t] = tb[oa[t]];
+            vb[t] = tb[ob[t]];
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            va[t] = tile.at(i, ca[t]);
+            vb[t] = tile.at(i, cb[t]);
+          }
+        }
+        uint32_t w0, w1, n0, n1;
+        top2(va, w0, n0);
+        top2(vb, w1, n1);
+        if (has_b) {
+          if ((reinterpret_cast<uintptr_t>(vrow) & 7) == 0) {
+            *reinterpret_cast<uint2*>(vrow) = make_uint2(w0, w1);
+          } else {
+            vrow[0] = w0;
+            vrow[1] = w1;
+          }
+          *mrow = static_cast<uint8_t>(n0 | (n1 << 4));
+        } else {
+          vrow[0] = w0;
+          *mrow = static_cast<uint8_t>(n0);
+        }
+      }
+      return;
+    }
+  }
+
   // ---- phase 3: thread per (row, group): the two largest |w| among the selected columns (2:4);
   // consecutive threads take consecutive groups of a row (coalesced value stores), the two
-  // nibbles of a metadata byte are joined with a lane shuffle
+  // nibbles of a metadata byte are joined with a lane shuffle. When the block size is a multiple
+  // of the row length a thread keeps one group and steps over rows (no divisions per item).
   const int per_row = ng + (ng & 1);  // even: lane pairs (2j, 2j+1) share a metadata byte
   const int work3 = (dbg & 4) ? 0 : V * per_row;
-  for (int w0 = 0; w0 < work3; w0 += blockDim.x) {
-    const int w = w0 + static_cast<int>(threadIdx.x);
+  const bool fixed_q = (nthr % per_row) == 0;
+  for (int w0 = 0; w0 < work3; w0 += nthr) {
+    const int w = w0 + tid;
     const bool act = w < work3;
-    const int i = act ? w / per_row : 0;
-    const int q = act ? w - i * per_row : 0;
+    const int i = !act ? 0 : (fixed_q ? (w0 / per_row) + tid / per_row : w / per_row);
+    const int q = !act ? 0 : (fixed_q ? tid % per_row : w - i * per_row);
     const bool live = act && q < ng;
     const int64_t row = row0 + i;
     uint32_t nibble = 0;
     if (live) {
       const uint32_t cw = s_sel[q];
-      const uint16_t* trow = tile + i * W + q * M;
+
       uint16_t v[4];
       uint32_t mag[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        v[t] = trow[(cw >> (8 * t)) & 0xFFu];
+        v[t] = tile.at(i, q * M + static_cast<int>((cw >> (8 * t)) & 0xFFu));
         mag[t] = v[t] & 0x7FFFu;  // |w| order for finite sign-magnitude formats; ±0 tie
       }
       // top-2 by (|a| desc, position asc) with register-only selects (no local-memory indexing)
@@ -477,6 +611,151 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
   }
 }
 
+template <bool kBF16, bool kExpand>
+__global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
+    const uint16_t* __restrict__ A, int64_t R, int64_t K, int64_t lda, int V, int M, int64_t G,
+    int gpc, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
+    uint8_t* __restrict__ column_idx, int32_t* __restrict__ status,
+    uint32_t* __restrict__ values2, uint32_t* __restrict__ meta_tc, int dbg) {
+  extern __shared__ __align__(16) uint8_t smem_dyn[];
+  uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const int64_t rb = blockIdx.y;
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * gpc;
+  const int ng = static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
+  const int W = gpc * M;                 // tile pitch (elements)
+  const int ncols = ng * M;
+  const int64_t k0 = g0 * M;
+  const int64_t row0 = rb * V;
+  const int64_t meta_row = (G + 1) / 2;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  constexpr int NS = CompressTileLayout::NS;
+  const CompressTileLayout lay(V, W, gpc, kExpand);
+  const int P = W + 8;                                                // padded row pitch
+  uint16_t* tile = reinterpret_cast<uint16_t*>(smem_raw + lay.tile);  // [V][W + 8]
+  float* s_part = reinterpret_cast<float*>(smem_raw + lay.part);       // [NS][W]
+  double* s_score = reinterpret_cast<double*>(smem_raw + lay.score);   // [W]
+  uint32_t* s_sel = reinterpret_cast<uint32_t*>(smem_raw + lay.sel);   // [gpc]
+  double* s_th = reinterpret_cast<double*>(smem_raw + lay.th);         // [gpc][2]: 4th, 5th score
+  uint8_t* s_rank = smem_raw + lay.rank;                               // [W]: selected?
+  // kExpand: the V:2:4 re-encoding's nibbles of this tile, [V][W/8] bytes (subgroups 2j, 2j+1)
+  uint8_t* s_m2 = smem_raw + lay.m2;
+
+  // ---- phase 0: the block tile, 16-byte loads (8 columns) where aligned, else element-wise. With
+  // a fixed (column vector, row) mapping per thread and 32-bit offsets from one base pointer, the
+  // whole tile is in flight at once for a handful of instructions per load. Non-finite inputs are
+  // detected from the column sums in phase 1 (an inf / nan makes its column's sum non-finite).
+  const int nvec = ncols / 8;  // full 8-column vectors of a row (W % 8 == 0 by construction)
+  const bool vec_ok = ((lda & 7) == 0) && ((k0 & 7) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  if (vec_ok && nvec > 0 && !(dbg & 1)) {
+    if (nthr % nvec == 0 && static_cast<int64_t>(V) * (lda / 8) < (int64_t(1) << 31)) {
+      constexpr int U = 8;
+      const int cv = tid % nvec, rstep = nthr / nvec, i0 = tid / nvec;
+      const uint32_t step = static_cast<uint32_t>(rstep * (lda / 8));  // uint4 per row step
+      const uint4* src = reinterpret_cast<const uint4*>(A + (row0 + i0) * lda + k0) + cv;
+      uint16_t* dst = tile + i0 * P + 8 * cv;
+      const int nload = i0 < V ? (V - i0 + rstep - 1) / rstep : 0;  // rows of this thread
+      for (int k = 0; k < nload; k += U) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (k + u < nload) w[u] = __ldcs(src + static_cast<uint32_t>(k + u) * step);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (k + u < nload) *reinterpret_cast<uint4*>(dst + (k + u) * rstep * P) = w[u];
+      }
+    } else {
+      constexpr int U = 4;
+      const int nv = V * nvec;
+      for (int t0 = tid; t0 < nv; t0 += U * nthr) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u * nthr;
+          if (t < nv) {
+            const int i = t / nvec, cv = t - i * nvec;
+            w[u] = __ldcs(reinterpret_cast<const uint4*>(A + (row0 + i) * lda + k0) + cv);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u * nthr;
+          if (t < nv) {
+            const int i = t / nvec, cv = t - i * nvec;
+            *reinterpret_cast<uint4*>(tile + i * P + 8 * cv) = w[u];
+          }
+        }
+      }
+    }
+  }
+  const int cstart = vec_ok ? 8 * nvec : 0;
+  const int ntail = ncols - cstart;
+  if (ntail > 0) {
+    for (int t = tid; t < V * ntail; t += nthr) {
+      const int i = t / ntail, c = cstart + (t - i * ntail);
+      tile[i * P + c] = __ldg(A + (row0 + i) * lda + k0 + c);
+    }
+  }
+  __syncthreads();
+
+  compress_tile_process<kBF16, kExpand>(TileView{tile, P, 0, false}, smem_raw, R, K, V, M, G, gpc, rb, g0, values,
+                                          metadata, column_idx, status, values2, meta_tc, dbg, 1);
+}
+
+// Compression, persistent TMA variant (the default when A is 16-byte aligned with a 16-byte row
+// pitch, V <= 256 and W % 64 == 0): one CTA per SM slot walks the (row block, column chunk) tiles in row-major
+// order; the V × W tile of the next two tiles is in flight (W / 64 TMA boxes of 64 columns with the
+// 128-byte swizzle each, double-buffered,
+// mbarrier-completed) while phases 1-4 run on the current one, so HBM streams continuously and
+// the per-CTA prologue is paid once (the one-tile-per-CTA kernel spent its time in load latency,
+// prologue and barriers: 0.61 ms for the GPT-3 FFN weight).
+template <bool kBF16, bool kExpand>
+__global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
+    const __grid_constant__ CUtensorMap tm_a, int64_t R, int64_t K, int V, int M, int64_t G, int gpc,
+    int64_t nchunks, int64_t ntiles, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
+    uint8_t* __restrict__ column_idx, int32_t* __restrict__ status, uint32_t* __restrict__ values2,
+    uint32_t* __restrict__ meta_tc, int dbg) {
+  using namespace ptx;
+  extern __shared__ __align__(16) uint8_t smem_dyn[];
+  uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[2];
+  const int W = gpc * M;
+  const CompressTileLayout lay(V, W, gpc, kExpand, 2, true);
+  const int nbox = (W + 63) / 64;
+  const uint32_t box_stride = static_cast<uint32_t>((V * 128 + 1023) & ~1023);  // bytes per 64-column box
+  const uint32_t tile_bytes = static_cast<uint32_t>(nbox) * V * 128;           // bytes the TMA delivers
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&full[0]), 1);
+    mbar_init(smem_u32(&full[1]), 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_a);
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int64_t t, int b) {  // thread 0: tile t -> buffer b
+    const int64_t rb = t / nchunks, cc = t - rb * nchunks;
+    mbar_arrive_expect_tx(smem_u32(&full[b]), tile_bytes);
+    for (int x = 0; x < nbox; ++x)
+      tma_load_2d(smem_u32(smem_raw + b * lay.tile_bytes + x * box_stride), &tm_a, smem_u32(&full[b]),
+                  static_cast<int32_t>(cc * W + 64 * x), static_cast<int32_t>(rb * V), pol);
+  };
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    if (t < ntiles) issue(t, 0);
+    if (t + gridDim.x < ntiles) issue(t + gridDim.x, 1);
+  }
+  for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    mbar_wait(smem_u32(&full[b]), (it >> 1) & 1);
+    const int64_t rb = t / nchunks, cc = t - rb * nchunks;
+    compress_tile_process<kBF16, kExpand>(TileView{reinterpret_cast<const uint16_t*>(smem_raw + b * lay.tile_bytes), 0,
+                                                   static_cast<int>(box_stride / 2), true}, smem_raw,
+                                          R, K, V, M, G, gpc, rb, cc * gpc, values, metadata, column_idx, status,
+                                          values2, meta_tc, dbg, 2);
+    __syncthreads();  // every thread is done with buffer b (and the scratch) before it is refilled
+    if (threadIdx.x == 0 && t + 2 * static_cast<int64_t>(gridDim.x) < ntiles) issue(t + 2 * static_cast<int64_t>(gridDim.x), b);
+  }
+}
+
 // Decompression: grid (column chunks, rows); thread per (row, kVec consecutive output elements).
 // Output +0.0 except the kept positions. Validates metadata when `status` is non-null. 32-bit
 // index arithmetic inside a row (K < 2^31), group/position advanced incrementally.
@@ -546,10 +825,12 @@ __global__ void __launch_bounds__(256) vnm_decompress_kernel(
 }
 
 // Decompression fast path for M % 8 == 0 (16-byte output vectors never straddle a group):
-// grid (chunk blocks, row slots); thread per (row, 8 outputs); the two kept positions are placed
-// with shifts, no per-element branches. CPG = M / 8 when it is a compile-time 1, 2 or 4, else 0
-// (runtime M).
-template <int CPG>
+// grid (chunk blocks, row slots); thread per (8 outputs of a row) for ROWS rows at a time, all of
+// their loads issued before any store (the loads of one row alone leave HBM idle: 1.9 TB/s at the
+// GPT-3 size). The two kept positions are placed with shifts, no per-element branches; the
+// streamed output is written with evict-first stores (it is not re-read by the step). CPG = M / 8
+// when it is a compile-time 1, 2 or 4, else 0 (runtime M).
+template <int CPG, int ROWS>
 __global__ void __launch_bounds__(256) vnm_decompress_m8_kernel(
     const uint32_t* __restrict__ values, const uint8_t* __restrict__ metadata,
     const uint32_t* __restrict__ column_idx, int R, int K, int V, int M, int G,
@@ -561,26 +842,51 @@ __global__ void __launch_bounds__(256) vnm_decompress_m8_kernel(
   const int cpg = CPG ? CPG : M / 8;  // 8-output chunks per group
   const int g = ch / cpg;
   const int j0 = (ch - g * cpg) * 8;  // first column of this chunk within the group
+  const bool same_block = (V % ROWS) == 0;  // the ROWS rows of a slot share column_idx
+  const bool check = status != nullptr;
   bool bad = false;
-  for (int row = blockIdx.y; row < R; row += gridDim.y) {
-    const uint32_t cw = __ldg(column_idx + (row / V) * G + g);
-    const uint32_t nib = (__ldg(metadata + static_cast<int64_t>(row) * meta_row + (g >> 1)) >> (4 * (g & 1))) & 0xFu;
-    const uint32_t vv = __ldg(values + static_cast<int64_t>(row) * G + g);
-    const uint32_t p0 = nib & 3u, p1 = nib >> 2;
-    bad |= !((cw & 0xFFu) < ((cw >> 8) & 0xFFu) && ((cw >> 8) & 0xFFu) < ((cw >> 16) & 0xFFu) &&
-             ((cw >> 16) & 0xFFu) < (cw >> 24) && (cw >> 24) < static_cast<uint32_t>(M)) ||
-           !(p0 < p1);
-    const int d0 = static_cast<int>((cw >> (8 * p0)) & 0xFFu) - j0;  // offsets inside the chunk
-    const int d1 = static_cast<int>((cw >> (8 * p1)) & 0xFFu) - j0;
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+  for (int row0 = blockIdx.y * ROWS; row0 < R; row0 += gridDim.y * ROWS) {
+    uint32_t cw[ROWS], nb[ROWS], vv[ROWS];
+    const int rb0 = row0 / V;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if ((d0 >> 1) == q) w[q] |= (vv & 0xFFFFu) << (16 * (d0 & 1));
-      if ((d1 >> 1) == q) w[q] |= (vv >> 16) << (16 * (d1 & 1));
+    for (int u = 0; u < ROWS; ++u) {
+      const int row = row0 + u;
+      cw[u] = 0x03020100u;
+      nb[u] = 0x4u;
+      vv[u] = 0u;
+      if (row < R) {
+        cw[u] = __ldg(column_idx + static_cast<int64_t>(same_block ? rb0 : row / V) * G + g);
+        nb[u] = __ldg(metadata + static_cast<int64_t>(row) * meta_row + (g >> 1));
+        vv[u] = __ldcs(values + static_cast<int64_t>(row) * G + g);
+      }
     }
-    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * lda + 8 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      const int row = row0 + u;
+      if (row >= R) break;
+      const uint32_t c = cw[u];
+      const uint32_t nib = (nb[u] >> (4 * (g & 1))) & 0xFu;
+      const uint32_t p0 = nib & 3u, p1 = nib >> 2;
+      if (check)
+        bad |= !((c & 0xFFu) < ((c >> 8) & 0xFFu) && ((c >> 8) & 0xFFu) < ((c >> 16) & 0xFFu) &&
+                 ((c >> 16) & 0xFFu) < (c >> 24) && (c >> 24) < static_cast<uint32_t>(M)) ||
+               !(p0 < p1);
+      // offsets of the two kept columns inside this 8-column chunk (outside [0, 8): not here);
+      // each lands in the low or high 64-bit half by a shift — no per-position branches
+      const uint32_t d0 = ((c >> (8 * p0)) & 0xFFu) - static_cast<uint32_t>(j0);
+      const uint32_t d1 = ((c >> (8 * p1)) & 0xFFu) - static_cast<uint32_t>(j0);
+      const uint64_t x0 = vv[u] & 0xFFFFu, x1 = vv[u] >> 16;
+      uint64_t lo = 0, hi = 0;
+      lo |= (d0 < 4u) ? (x0 << (16 * d0)) : 0ull;
+      hi |= (d0 - 4u < 4u) ? (x0 << (16 * (d0 - 4u))) : 0ull;
+      lo |= (d1 < 4u) ? (x1 << (16 * d1)) : 0ull;
+      hi |= (d1 - 4u < 4u) ? (x1 << (16 * (d1 - 4u))) : 0ull;
+      __stcs(reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * lda + 8 * ch),
+             make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32), static_cast<uint32_t>(hi),
+                        static_cast<uint32_t>(hi >> 32)));
+    }
   }
-  if (bad && status != nullptr) atomicMax(status, kStatusCorruptMetadata);
+  if (bad) atomicMax(status, kStatusCorruptMetadata);
 }
 
 // Re-encoding V:N:M (M % 4 == 0) -> V:2:4 over the original K (reading #18; the oracle's

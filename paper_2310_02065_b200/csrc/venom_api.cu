@@ -54,7 +54,16 @@ venom_status_t validate_format(int64_t R, int64_t K, venom_format_t f) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-constexpr int kCompressThreads = 512;
+// compressor tile kernel: threads per CTA and the largest V × W tile (bytes); a smaller tile with
+// fewer threads keeps more independent CTAs per SM (their load and compute phases overlap)
+#ifndef VENOM_COMPRESS_THREADS
+#define VENOM_COMPRESS_THREADS 256
+#endif
+#ifndef VENOM_COMPRESS_TILE_BYTES
+#define VENOM_COMPRESS_TILE_BYTES 32768
+#endif
+constexpr int kCompressThreads = VENOM_COMPRESS_THREADS;
+constexpr int64_t kCompressTileBytes = VENOM_COMPRESS_TILE_BYTES;
 
 // ablation flags for the analysis tools (VENOM_DEBUG_FLAGS): honoured only by the separate
 // -DVENOM_ABLATION build (libvenom_ablation.so); the production library always passes 0
@@ -65,6 +74,43 @@ int debug_flags() {
 #else
   return 0;
 #endif
+}
+
+// The persistent TMA compressor applies when A can be described by a tensor map (16-byte aligned
+// base and row pitch) and the V × W tile is one TMA box (each box dimension <= 256 elements).
+bool tma_compress_ok(const void* A, int64_t lda, int V, int W) {
+  return aligned(A, 16) && (lda % 8 == 0) && V <= 256 && W <= 256 && (W % 64 == 0) && encode_fn() != nullptr;
+}
+
+template <typename Kern>
+venom_status_t launch_compress_tma(Kern kern, const void* A, int64_t R, int64_t K, int64_t lda, venom_format_t f,
+                                   int gt, bool expand, void* values, uint8_t* metadata, uint8_t* column_idx,
+                                   int32_t* dev_status, uint32_t* values2, uint32_t* meta_tc, cudaStream_t s) {
+  const int W = gt * f.m;
+  const int64_t G = K / f.m;
+  CUtensorMap tm;
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * lda)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(f.v)};  // 64-column boxes, 128-byte swizzle
+    cuuint32_t es[2] = {1, 1};
+    if (encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(A), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return VENOM_ERR_CUDA;
+  }
+  const size_t smem = venom::CompressTileLayout(f.v, W, gt, expand, 2, true).total;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    return VENOM_ERR_CUDA;
+  const int64_t nchunks = (G + gt - 1) / gt, ntiles = nchunks * (R / f.v);
+  int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
+  if (per_sm > 8) per_sm = 8;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = static_cast<int64_t>(venom::launch::sm_count()) * per_sm;
+  const unsigned grid = static_cast<unsigned>(ntiles < cap ? ntiles : cap);
+  kern<<<grid, 256, smem, s>>>(tm, R, K, f.v, f.m, G, gt, nchunks, ntiles, static_cast<uint16_t*>(values), metadata,
+                               column_idx, dev_status, values2, meta_tc, debug_flags());
+  return launch_status();
 }
 
 }  // namespace
@@ -116,33 +162,46 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
   if ((st = check_arch()) != VENOM_OK) return st;
   const int64_t G = K / f.m;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nrb = R / f.v;
+  // grid.y is limited to 65535: row blocks beyond it are compressed by further launches on
+  // row-offset views (every kernel addresses rows relative to its pointers)
+  constexpr int64_t kMaxRowBlocks = 65535;
   {
     // shared-memory tile kernel: ~256 columns per CTA (even number of groups, W % 8 == 0), the
-    // V × W tile at most 64 KB; narrower chunks when the grid would have < 2 CTAs per SM
+    // V × W tile at most kCompressTileBytes; narrower chunks when the grid would have < 2 CTAs per SM
     int gt = 256 / f.m;
     gt -= gt & 1;
     if (gt < 2) gt = 2;
     while ((gt * f.m) % 8 != 0) gt += 2;
-    while (gt > 2 && static_cast<int64_t>(f.v) * gt * f.m * 2 > 65536) gt -= 2;
+    while (gt > 2 && static_cast<int64_t>(f.v) * gt * f.m * 2 > kCompressTileBytes) gt -= 2;
     while ((gt * f.m) % 8 != 0 && gt > 2) gt -= 2;
     if (gt > G + (G & 1)) gt = static_cast<int>(G + (G & 1));
     while ((gt * f.m) % 8 != 0) gt += 2;  // pitch alignment (may exceed G: extra columns unused)
-    while (gt >= 8 && ((G + gt - 1) / gt) * (R / f.v) < 2 * 148 && ((gt / 2) * f.m) % 8 == 0 &&
-           (gt / 2) % 2 == 0)
+    while (gt >= 8 && ((G + gt - 1) / gt) * nrb < 2 * 148 && ((gt / 2) * f.m) % 8 == 0 && (gt / 2) % 2 == 0)
       gt /= 2;
-    const size_t tsmem = ((static_cast<size_t>(f.v) * gt * f.m * 2 + 15) & ~size_t(15)) +
-                         8 * static_cast<size_t>(gt) * f.m + 4 * static_cast<size_t>(gt) + 16 +
-                         16 * static_cast<size_t>(gt) * f.m;  // + fp16 row-half partial sums
-    if (tsmem <= 100 * 1024 && (R / f.v) <= 65535) {
-      const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
+    const size_t tsmem = venom::CompressTileLayout(f.v, gt * f.m, gt, false).total;
+    if (tsmem <= 100 * 1024 && tma_compress_ok(A, lda, f.v, gt * f.m)) {
+      auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, false>
+                                     : venom::vnm_compress_tma_kernel<false, false>;
+      return launch_compress_tma(kern, A, R, K, lda, f, gt, false, values, metadata, column_idx, dev_status,
+                                 nullptr, nullptr, s);
+    }
+    if (tsmem <= 100 * 1024) {
       auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, false>
                                      : venom::vnm_compress_tile_kernel<false, false>;
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)) != cudaSuccess)
         return VENOM_ERR_CUDA;
-      kern<<<grid, kCompressThreads, tsmem, s>>>(static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gt,
-                                    static_cast<uint16_t*>(values), metadata, column_idx, dev_status,
-                                    nullptr, nullptr, debug_flags());
-      return launch_status();
+      for (int64_t rb0 = 0; rb0 < nrb; rb0 += kMaxRowBlocks) {
+        const int64_t nb = (nrb - rb0) < kMaxRowBlocks ? (nrb - rb0) : kMaxRowBlocks;
+        const int64_t r0 = rb0 * f.v;
+        const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(nb));
+        kern<<<grid, kCompressThreads, tsmem, s>>>(
+            static_cast<const uint16_t*>(A) + r0 * lda, nb * f.v, K, lda, f.v, f.m, G, gt,
+            static_cast<uint16_t*>(values) + r0 * G * 2, metadata + r0 * ((G + 1) / 2), column_idx + rb0 * G * 4,
+            dev_status, nullptr, nullptr, debug_flags());
+        if ((st = launch_status()) != VENOM_OK) return st;
+      }
+      return VENOM_OK;
     }
   }
   // very tall blocks: streaming kernel (partial sums over row ranges, no tile copy)
@@ -152,26 +211,32 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
   if (gpc < 2) gpc = 2;
   if (gpc > G + (G & 1)) gpc = static_cast<int>(G + (G & 1));
   // latency hiding: at least ~4 CTAs per SM (narrower column chunks when R/V × K/256 is small)
-  while (gpc >= 4 && ((G + gpc - 1) / gpc) * (R / f.v) < 4 * 148) gpc = (gpc / 2) & ~1;
+  while (gpc >= 4 && ((G + gpc - 1) / gpc) * nrb < 4 * 148) gpc = (gpc / 2) & ~1;
   const bool vec = aligned(A, 16) && (lda % 8 == 0) && ((static_cast<int64_t>(gpc) * f.m) % 8 == 0);
-  const dim3 grid(static_cast<unsigned>((G + gpc - 1) / gpc), static_cast<unsigned>(R / f.v));
-  if (grid.y > 65535u) return VENOM_ERR_INVALID_ARGUMENT;
   const int wmax = gpc * f.m;
   const int vecw = vec ? 8 : 1;
   const int ncv_max = (wmax + vecw - 1) / vecw;
   const int nsplit_max = (dt == VENOM_BF16) ? 1 : (256 / ncv_max > 0 ? 256 / ncv_max : 1);
   const size_t smem = sizeof(double) * static_cast<size_t>(nsplit_max) * wmax + 4 * static_cast<size_t>(gpc);
-#define VENOM_COMPRESS(BF, VW)                                                                     \
-  venom::vnm_compress_kernel<BF, VW><<<grid, 256, smem, s>>>(                                      \
-      static_cast<const uint16_t*>(A), R, K, lda, f.v, f.m, G, gpc, static_cast<uint16_t*>(values), \
-      metadata, column_idx, dev_status)
-  if (dt == VENOM_BF16) {
-    if (vec) VENOM_COMPRESS(true, 8); else VENOM_COMPRESS(true, 1);
-  } else {
-    if (vec) VENOM_COMPRESS(false, 8); else VENOM_COMPRESS(false, 1);
-  }
+  for (int64_t rb0 = 0; rb0 < nrb; rb0 += kMaxRowBlocks) {
+    const int64_t nb = (nrb - rb0) < kMaxRowBlocks ? (nrb - rb0) : kMaxRowBlocks;
+    const int64_t r0 = rb0 * f.v;
+    const dim3 grid(static_cast<unsigned>((G + gpc - 1) / gpc), static_cast<unsigned>(nb));
+    const uint16_t* Ar = static_cast<const uint16_t*>(A) + r0 * lda;
+    uint16_t* vr = static_cast<uint16_t*>(values) + r0 * G * 2;
+    uint8_t* mr = metadata + r0 * ((G + 1) / 2);
+    uint8_t* cr = column_idx + rb0 * G * 4;
+#define VENOM_COMPRESS(BF, VW) \
+  venom::vnm_compress_kernel<BF, VW><<<grid, 256, smem, s>>>(Ar, nb * f.v, K, lda, f.v, f.m, G, gpc, vr, mr, cr, dev_status)
+    if (dt == VENOM_BF16) {
+      if (vec) VENOM_COMPRESS(true, 8); else VENOM_COMPRESS(true, 1);
+    } else {
+      if (vec) VENOM_COMPRESS(false, 8); else VENOM_COMPRESS(false, 1);
+    }
 #undef VENOM_COMPRESS
-  return launch_status();
+    if ((st = launch_status()) != VENOM_OK) return st;
+  }
+  return VENOM_OK;
 }
 
 venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t lda, venom_dtype_t dt,
@@ -197,9 +262,14 @@ venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t 
   const int W = (f.v <= 128 && !(debug_flags() & 16)) ? 256 : 128;
   const int gt = W / f.m > 0 ? W / f.m : 1;
   if (gt * f.m != W) return VENOM_ERR_UNSUPPORTED_PATTERN;  // M must divide W (M | 128)
-  const size_t tsmem = ((static_cast<size_t>(f.v) * W * 2 + 15) & ~size_t(15)) + 8 * static_cast<size_t>(W) +
-                       4 * static_cast<size_t>(gt) + static_cast<size_t>(f.v) * (W / 8) + 16 +
-                       16 * static_cast<size_t>(W);  // + fp16 row-half partial sums
+  const size_t tsmem = venom::CompressTileLayout(f.v, W, gt, true).total;
+  if (tma_compress_ok(A, lda, f.v, W) && !(debug_flags() & 32)) {
+    auto kt = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, true>
+                                 : venom::vnm_compress_tma_kernel<false, true>;
+    return launch_compress_tma(kt, A, R, K, lda, f, gt, true, values, metadata, column_idx, dev_status,
+                               static_cast<uint32_t*>(values_2to4), reinterpret_cast<uint32_t*>(metadata_2to4_tc),
+                               static_cast<cudaStream_t>(stream));
+  }
   const dim3 grid(static_cast<unsigned>((G + gt - 1) / gt), static_cast<unsigned>(R / f.v));
   auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tile_kernel<true, true>
                                  : venom::vnm_compress_tile_kernel<false, true>;
@@ -285,9 +355,11 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
   const int64_t blocks = (R * chunks + 255) / 256;
   const dim3 grid(static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64));
   if (vec && f.m % 8 == 0 && R <= 0x7FFFFFFF) {
-    const dim3 g2(static_cast<unsigned>((K / 8 + 255) / 256), static_cast<unsigned>(R < 65535 ? R : 65535));
+    constexpr int kRows = 4;  // rows per thread (loads of all of them in flight together)
+    const int64_t slots = (R + kRows - 1) / kRows;
+    const dim3 g2(static_cast<unsigned>((K / 8 + 255) / 256), static_cast<unsigned>(slots < 65535 ? slots : 65535));
 #define VENOM_DEC8(C)                                                                                  \
-  venom::vnm_decompress_m8_kernel<C><<<g2, 256, 0, s>>>(                                               \
+  venom::vnm_decompress_m8_kernel<C, kRows><<<g2, 256, 0, s>>>(                                        \
       static_cast<const uint32_t*>(values), metadata, reinterpret_cast<const uint32_t*>(column_idx), \
       static_cast<int>(R), static_cast<int>(K), f.v, f.m, static_cast<int>(G),                        \
       static_cast<uint16_t*>(A_out), lda, dev_status)

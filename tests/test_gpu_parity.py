@@ -85,6 +85,88 @@ def test_compress_bit_exact(R, K, V, M, kind, dt):
         assert np.array_equal(g.reshape(e.shape), e), name
 
 
+# shapes whose V × W tile exceeds the shared-memory tile kernel's budget: the streaming compressor
+# (vnm_compress_kernel, row-split fp64 partial sums) — fp16 and bf16, odd G, 16-byte vector and
+# element-wise loads (an lda view that is not a multiple of 8)
+STREAM_CASES = [
+    # (R, K, V, M, kind, dt, lda_pad)
+    (512, 1024, 256, 128, "gauss", F16, 0),
+    (1024, 2048, 1024, 32, "int", BF16, 0),
+    (512, 384, 256, 128, "special", F16, 0),      # G = 3 (odd)
+    (512, 1024, 256, 128, "gauss", BF16, 3),      # lda % 8 != 0: element-wise loads
+    (2048, 512, 2048, 64, "sparse", F16, 5),
+]
+
+
+@pytest.mark.parametrize("R,K,V,M,kind,dt,pad", STREAM_CASES)
+def test_compress_streaming_kernel_bit_exact(R, K, V, M, kind, dt, pad):
+    A = make_input(R, K + pad, kind, dt, 2000 + R + K + V + M + pad, M)
+    x = venom.compress(to_dev(A, dt)[:, :K], V=V, M=M, check=True)
+    exp = oracle.compress(np.ascontiguousarray(A[:, :K]), dt, V=V, M=M)
+    got = (to_bits(x.values), x.metadata.cpu().numpy(), x.column_idx.cpu().numpy())
+    for name, g, e in zip(("values", "metadata", "column_idx"), got, exp):
+        assert np.array_equal(g.reshape(e.shape), e), name
+
+
+def near_tie_input(R, K, V, M, dt, seed):
+    """Every column of a V-row block has the same bulk (V - 1 entries of 1.0) plus one tiny entry
+    whose size decides the column order: the column sums differ by far less than an fp32 sum can
+    resolve, so the compressor's approximate scores cannot decide the top-4 and its exact path
+    must (fp16: subnormal steps of 2^-24; bf16: steps of 2^-16 on top of 1.0 entries)."""
+    rng = np.random.default_rng(seed)
+    one = 0x3C00 if dt == F16 else 0x3F80
+    A = np.full((R, K), one, np.uint16)
+    for rb in range(R // V):
+        for g in range(K // M):
+            perm = rng.permutation(M) + 1
+            r = rb * V + int(rng.integers(0, V))
+            tiny = perm.astype(np.uint16) if dt == F16 else (0x3780 + perm).astype(np.uint16)  # bf16 ~2^-16·k
+            A[r, g * M:(g + 1) * M] = tiny
+    return A
+
+
+@pytest.mark.parametrize("R,K,V,M,dt", [(256, 1024, 128, 16, F16), (128, 512, 64, 8, BF16),
+                                        (64, 640, 32, 40, F16), (128, 256, 128, 32, F16)])
+def test_compress_near_ties_bit_exact(R, K, V, M, dt):
+    A = near_tie_input(R, K, V, M, dt, 11 + R + M)
+    exp = oracle.compress(A, dt, V=V, M=M)
+    _, got = gpu_compress(A, dt, V, M)
+    for name, g, e in zip(("values", "metadata", "column_idx"), got, exp):
+        assert np.array_equal(g.reshape(e.shape), e), name
+    if M % 8 == 0 and 128 % M == 0 and V % 16 == 0:  # the fused compress + V:2:4 path decides alike
+        x2, _ = venom.compress_2to4(to_dev(A, dt), V=V, M=M, check=True)
+        assert np.array_equal(x2.column_idx.cpu().numpy(), exp[2])
+
+
+@pytest.mark.parametrize("R,K,V,M,dt", [(3072, 4096, 128, 16, F16), (2048, 2048, 64, 8, BF16),
+                                        (512, 8192, 256, 32, F16)])
+def test_compress_many_tiles_per_cta(R, K, V, M, dt):
+    """More (row block, column chunk) tiles than the persistent compressor has CTAs: every CTA runs
+    its double-buffered TMA pipeline over several tiles (GPT-3-like aspect, scaled down); the fused
+    compress + V:2:4 kernel takes the same path."""
+    A = synth.gaussian((R, K), 0.02, dt, 5 + R + M)
+    exp = oracle.compress(A, dt, V=V, M=M)
+    _, got = gpu_compress(A, dt, V, M)
+    for name, g, e in zip(("values", "metadata", "column_idx"), got, exp):
+        assert np.array_equal(g.reshape(e.shape), e), name
+    if M % 8 == 0 and 128 % M == 0 and V % 16 == 0:
+        x2, y2 = venom.compress_2to4(to_dev(A, dt), V=V, M=M, check=True)
+        assert np.array_equal(to_bits(x2.values).reshape(exp[0].shape), exp[0])
+        assert np.array_equal(x2.column_idx.cpu().numpy(), exp[2])
+        exp2 = oracle.expand_2to4(*exp, R, K, V, M)
+        assert np.array_equal(to_bits(y2.values).reshape(exp2[0].shape), exp2[0])
+
+
+def test_compress_more_than_65535_row_blocks():
+    """V = 1 with R > 65535: the row blocks exceed one launch's grid.y (chunked launches)."""
+    R, K, V, M = 70000, 32, 1, 8
+    A = synth.gaussian((R, K), 0.02, F16, 77)
+    exp = oracle.compress(A, F16, V=V, M=M)
+    _, got = gpu_compress(A, F16, V, M)
+    for name, g, e in zip(("values", "metadata", "column_idx"), got, exp):
+        assert np.array_equal(g.reshape(e.shape), e), name
+
+
 @pytest.mark.parametrize("name", ["P1_spec_worked_example.json", "P2_greedy_not_joint.json",
                                   "P3_fp64_exact_column_sums.json", "P4_raw_bits_and_zero_ties.json"])
 def test_compress_golden_on_gpu(name):
@@ -302,10 +384,12 @@ def test_spmm_densek_vs_oracle(R, K, T, V, M, dt, bias):
     A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 700 + R + K + T + M, bias)
     C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
     x = vnm_from(parts, R, K, V, M, dt)
-    for tt in (0, 128):
-        C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tt,
-                       strategy=venom.STRATEGY_DENSE_K)
-        check_spmm(C, C_ref, dt)
+    # the default CTA pair and the single-CTA instantiations (cta_pair = 1), both tile widths
+    for pair in (0, 1):
+        for tt in (0, 128):
+            C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt) if bias else None, tile_t=tt,
+                           strategy=venom.STRATEGY_DENSE_K, cta_pair=pair)
+            check_spmm(C, C_ref, dt)
 
 
 def test_spmm_identity_probe_exact_densek():
@@ -827,3 +911,47 @@ def test_tensor_parallel_allgather_on_gpu():
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_spmm_argument_errors_are_synchronous():
+    """out-of-range cta_pair, a non-zero stages override and misaligned metadata /
+    column_idx views return VENOM_ERR_INVALID_ARGUMENT before anything is launched."""
+    R, K, T, V, M = 256, 512, 64, 128, 16
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, F16, 5, False)
+    x = vnm_from(parts, R, K, V, M, F16)
+    Bd = to_dev(B, F16)
+    for kw in (dict(cta_pair=3), dict(cta_pair=-1), dict(stages=2)):
+        with pytest.raises(venom.VenomError) as ei:
+            venom.spmm(x, Bd, **kw)
+        assert ei.value.status == 1, kw
+    # a metadata view that is only 1-byte aligned (canonical metadata is read with 16-byte loads)
+    meta_buf = torch.zeros(x.metadata.numel() + 16, dtype=torch.uint8, device=Bd.device)
+    meta_view = meta_buf[1:1 + x.metadata.numel()].view(x.metadata.shape)
+    meta_view.copy_(x.metadata)
+    y = venom.VNMTensor(x.values, meta_view, x.column_idx, R, K, V, M)
+    with pytest.raises(venom.VenomError) as ei:
+        venom.spmm(y, Bd, use_metadata_tc=False)
+    assert ei.value.status == 1
+    # dense-K reads column_idx with 16-byte loads: a 4-byte-aligned view is refused there
+    cbuf = torch.zeros(x.column_idx.numel() + 16, dtype=torch.uint8, device=Bd.device)
+    cview = cbuf[4:4 + x.column_idx.numel()].view(x.column_idx.shape)
+    cview.copy_(x.column_idx)
+    z = venom.VNMTensor(x.values, x.metadata, cview, R, K, V, M)
+    with pytest.raises(venom.VenomError) as ei:
+        venom.spmm(z, Bd, strategy=venom.STRATEGY_DENSE_K)
+    assert ei.value.status == 1
+    torch.cuda.synchronize()
+
+
+def test_compress_out_refreshes_tensor_core_metadata():
+    """compress(A, out=x) on an operand that carries tensor-core-ordered metadata
+    re-derives it, so spmm(x, B) pairs the new values with the new m-indices."""
+    R, K, T, V, M = 256, 1024, 128, 128, 16
+    A1 = synth.gaussian((R, K), 0.02, F16, 41)
+    A2 = synth.gaussian((R, K), 0.02, F16, 42)
+    B = synth.gaussian((K, T), 1.0, F16, 43)
+    x = venom.order_metadata(venom.compress(to_dev(A1, F16), V=V, M=M))
+    venom.compress(to_dev(A2, F16), V=V, M=M, out=x)
+    C = venom.spmm(x, to_dev(B, F16))  # uses x.metadata_tc
+    parts = oracle.compress(A2, F16, V=V, M=M)
+    check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, B), F16)

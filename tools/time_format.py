@@ -4,7 +4,8 @@ import os, sys, statistics
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2310_02065_b200.build import build as _build
-os.environ.setdefault("VENOM_LIB", _build(ablation=True))  # the build that honours VENOM_DEBUG_FLAGS
+if os.environ.get("ABLATE"):
+    os.environ.setdefault("VENOM_LIB", _build(ablation=True))  # the build that honours VENOM_DEBUG_FLAGS
 import paper_2310_02065_b200 as venom
 
 R, K, V, M = (int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (1024, 4096, 64, 8)))
