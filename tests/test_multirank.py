@@ -42,6 +42,26 @@ def _worker(rank: int, ws: int, port: int, q):
         assert bench.aggregate(10.0, ws, t) == pytest.approx(10.0 * ws / t)
         bench.barrier(ws)
 
+        # strong scaling (bench.py --scaling strong, the default): bench.shard gives rank r the
+        # columns [t0, t1) of the one global B and the rows [r0, r1) it decompresses; over the ranks
+        # the column slices tile [0, T) and the row slices tile [0, R) in whole V-blocks
+        w = dict(R=12288, K=49152, T=8192, V=128, M=16)
+        sh = bench.shard(w, ws, rank, "strong")
+        all_sh = [None] * ws
+        dist.all_gather_object(all_sh, sh)
+        assert [a[0] for a in all_sh] == [r * (8192 // ws) for r in range(ws)]
+        assert all_sh[-1][1] == 8192 and all(all_sh[r][1] == all_sh[r + 1][0] for r in range(ws - 1))
+        assert all_sh[0][2] == 0 and all_sh[-1][3] == 12288
+        assert all(all_sh[r][3] == all_sh[r + 1][2] for r in range(ws - 1)) and all(a[2] % 128 == 0 for a in all_sh)
+        assert bench.shard(w, ws, rank, "weak") == (0, 8192, 0, 12288)
+        with pytest.raises(ValueError):
+            bench.shard(dict(w, T=8 * ws + 4), ws, rank, "strong")
+        # the job's useful FLOPs: strong-split ranks add up to the unsharded layer
+        per_rank = bench.useful_flops(w, sh[1] - sh[0])
+        tot = torch.tensor([per_rank], dtype=torch.float64)
+        dist.all_reduce(tot)
+        assert float(tot) == bench.useful_flops(w)
+
         # T-split: rank r owns columns [r*T/ws, (r+1)*T/ws) of one global B; no collective on the
         # SpMM itself, the all_gather below only collects the result for the check
         R, K, T, V, M = 64, 128, 96, 32, 8

@@ -1,6 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
 W=gpt3_ffn_12288x49152x8192_128:2:16
-for lib in libvenom_r1.so libvenom_p8.so libvenom.so libvenom_r1.so; do
-  VENOM_LIB=paper_2310_02065_b200/$lib timeout 300 python tools/time_spmm.py $W group_n=1 group_n=3
-done 2>&1 | grep -v Warn
+for lib in libvenom.so libvenom_p11.so libvenom.so; do
+  VENOM_LIB=paper_2310_02065_b200/$lib timeout 60 python tools/time_spmm.py $W "" 2>&1 | grep -v Warn | tail -1
+done
+VENOM_LIB=paper_2310_02065_b200/libvenom.so timeout 300 python -m pytest tests -q -m gpu -x -k "spmm" 2>&1 | tail -2
