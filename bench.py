@@ -60,11 +60,13 @@ for _k in synth.WORKLOADS:
 DEFAULT_WORKLOAD = "gpt3_ffn_12288x49152x8192_128:2:16"
 SECONDARY_WORKLOAD = "bert_large_ffn_4096tok_64:2:8"  # BASELINE configs[1]
 
-# Per-SM L2 -> SMEM landing ceiling (GB/s per SM) for the `feed` roofline: the independent TMA
-# microbenchmark (tools/microbench_feed.cu, profiles/r02_microbench_feed.txt) — 4 KB tile boxes
-# with >= 160 KB in flight per SM on all 148 SMs, no MMA.
-FEED_CEILING_GBPS_PER_SM = 118.0
-FEED_CEILING_SOURCE = "tools/microbench_feed.cu (TMA tile boxes, 148 SMs, no MMA; profiles/r02_microbench_feed.txt)"
+# Per-SM L2 -> SMEM landing ceiling (GB/s per SM) for the `feed` roofline, from the independent TMA
+# microbenchmark (tools/microbench_feed.cu, profiles/r02_microbench_feed.txt): the best rate of
+# contiguous tile boxes with 160 KB in flight per SM on all 148 SMs, no MMA (153 B/ns per SM;
+# 110 B/ns with the sparse MMA reading the same shared memory; tile::gather4 rows reach 84 B/ns).
+FEED_CEILING_GBPS_PER_SM = 153.0
+FEED_CEILING_SOURCE = ("tools/microbench_feed.cu: TMA tile boxes, 148 SMs, 160 KB in flight per SM, no MMA "
+                       "(profiles/r02_microbench_feed.txt; gather4 rows: 84 B/ns per SM)")
 
 
 def useful_flops(w, T=None) -> float:
