@@ -276,7 +276,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     int m_tile, n_tile;
     tile_coords<CG>(p, tl, m_tile, n_tile);
     const int ab = tl % Cfg::ACC_BUFS;
-    mbar_wait(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);
+    mbar_wait_sleep(accf0 + 8 * ab, (tl / Cfg::ACC_BUFS) & 1);  // a whole tile: sleep, do not poll
     tc_fence_after();
     if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row = static_cast<int64_t>(m_tile) * (128 * CG) + r_local;
@@ -397,7 +397,7 @@ __device__ __forceinline__ void epilogue_role_mb2(const SpmmParams& p, int my_ti
   for (int tl = 0; tl < my_tiles; ++tl) {
     int m_tile, n_tile;
     tile_coords<CG>(p, tl, m_tile, n_tile);
-    mbar_wait(accf0, tl & 1);
+    mbar_wait_sleep(accf0, tl & 1);
     tc_fence_after();
     if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG * 2) + b * (128 * CG) +
