@@ -55,6 +55,7 @@ struct DenseKCfg {
   // expanders load the values straight from global memory (true) or from the TMA values ring
   static constexpr bool DIRECT = true;
   static constexpr int W_MMA = 1, W_RAW = 2, W_EPI = 4, W_EXP = 8, N_EXP = 8, EPI_WARPS = 4;
+  static constexpr int EPI_SLOT = 2048, EPI_BUFS = 1;  // (the shared epilogue's TMA-store path is unused here)
   static constexpr int NUM_THREADS = 32 * (W_EXP + N_EXP);
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + RS * RAW_BYTES + 512;
   static_assert(M_ % 4 == 0 && M_ <= 32, "dense-K: M in {4, 8, 16, 32}");

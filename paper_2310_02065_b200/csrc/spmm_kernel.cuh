@@ -52,6 +52,7 @@ struct SpmmParams {
   int c_t;  // C stored transposed (token-major): element (r, t) at C[t * ldc + r]
   int bk;   // B given K-major (token-major activations, dtype[T][ldb]); M = 4 operand only
   int act;  // 1: GELU after the bias (row-major C only)
+  int tma_c;  // row-major C stored by TMA boxes (tm_c encoded by the host)
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -95,9 +96,13 @@ struct SpmmCfg {
   static constexpr int W_MMA = P, W_EPI = P + 1, W_META = P + 1 + EPI_WARPS;
   static constexpr int NUM_THREADS = 32 * (P + 1 + EPI_WARPS + (PRE_ ? 0 : 4));
   static_assert(CG_ == 1 || NB_ == 1, "CTA pairs need one V-block per CTA tile");
-  static constexpr int BAR_BYTES = 256;
-  // per epilogue warp: one 32-row output chunk (64 B rows; 32 B rows for MB = 2)
-  static constexpr int EPI_STAGE_BYTES = (MB_ == 2) ? 1024 : 2048;
+  static constexpr int BAR_BYTES = 1024;  // keeps the epilogue slots 1 KB aligned (TMA-store swizzle)
+  // per epilogue warp: one 32-row output chunk (64 B rows; 32 B rows for MB = 2); MB = 1 stages its
+  // chunks for TMA stores, double-buffered when the shared memory allows
+  static constexpr int EPI_SLOT = (MB_ == 2) ? 1024 : 2048;
+  static constexpr int EPI_BUFS =
+      (MB_ == 1 && 1024 + STAGES_ * STAGE_BYTES + BAR_BYTES + EPI_WARPS * 2 * EPI_SLOT <= 227 * 1024) ? 2 : 1;
+  static constexpr int EPI_STAGE_BYTES = EPI_SLOT * EPI_BUFS;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_WARPS * EPI_STAGE_BYTES;
   static_assert((BNH % 64 == 0 || MB_ == 2) && BNH % 8 == 0 && BN <= 256, "BN");
   static_assert(MB_ == 1 || (CG_ == 2 && NB_ == 1 && PRE_), "two row blocks: CTA pair, pre-ordered metadata");
@@ -263,7 +268,7 @@ __device__ __forceinline__ float gelu_f(float v) { return 0.5f * v * (1.0f + erf
 template <class Cfg, bool kBF16, int CG = 1, bool kCT = false, bool kGELU = false>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane,
-                                              uint32_t stage_smem = 0) {
+                                              uint32_t stage_smem = 0, const CUtensorMap* tm_c = nullptr) {
   using namespace ptx;
   constexpr int NB = Cfg::NB, BN = Cfg::BN;
   constexpr int HC = BN / (Cfg::EPI_WARPS / 4);  // columns per warp
@@ -335,6 +340,37 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
           }
         }
     } else if (p.dbg & 4) {  // ablation 4: no C stores
+    } else if (tm_c != nullptr && !(p.dbg & 16384)) {
+      // TMA-store epilogue (the paper's stage 3 output staging, on the bulk-copy
+      // engine): each 32-row × 32-column chunk is written to a shared-memory slot in the 64-byte
+      // swizzled layout of the C tensor map (16-byte segment s of row r at segment s ^ ((r >> 1) & 3),
+      // conflict-free), then one lane stores the box with cp.async.bulk.tensor; the TMA unit
+      // clips the ragged R / T edges. Slots are double-buffered when shared memory allows: a slot
+      // is rewritten only once the store issued from it has read it.
+      const int row_base = m_tile * (128 * CG) + 128 * static_cast<int>(rank) + 32 * q;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (32 * c >= HC) break;
+        const uint32_t slot = stage_smem + (c % Cfg::EPI_BUFS) * Cfg::EPI_SLOT;
+        if (lane == 0) {
+          if (Cfg::EPI_BUFS == 2) bulk_wait_group_read<1>();
+          else bulk_wait_group_read<0>();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int sgm = 0; sgm < 4; ++sgm) {
+          const uint32_t a = slot + lane * 64 + ((sgm ^ ((lane >> 1) & 3)) * 16);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c][4 * sgm]),
+                       "r"(pk[c][4 * sgm + 1]), "r"(pk[c][4 * sgm + 2]), "r"(pk[c][4 * sgm + 3]) : "memory");
+        }
+        fence_proxy_async_smem();  // the generic-proxy writes, visible to the bulk-copy engine
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(tm_c, slot, static_cast<int32_t>(col_base + 32 * c), row_base);
+          bulk_commit_group();
+        }
+      }
+      if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(10, tl);
     } else if (stage_smem != 0 && !(p.dbg & 16384)) {  // ablation 16384: direct stores below
       // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
       // store instruction writes 8 rows × 64 contiguous bytes (full sectors) instead of 32 rows ×
@@ -375,6 +411,8 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
                 make_uint4(pk[c][4 * u], pk[c][4 * u + 1], pk[c][4 * u + 2], pk[c][4 * u + 3]);
     }
   }
+  // the CTA's shared memory must outlive the stores that read it
+  if (tm_c != nullptr && lane == 0) bulk_wait_group_all();
 }
 
 // Epilogue for MB = 2 (two 128-row accumulators per CTA, BN = 240): 16 warps, warp e = w - W_EPI
@@ -548,7 +586,8 @@ template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false, bool 
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
-                    const __grid_constant__ CUtensorMap tm_e, const SpmmParams p) {
+                    const __grid_constant__ CUtensorMap tm_e,
+                    const __grid_constant__ CUtensorMap tm_c, const SpmmParams p) {
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN, CG = Cfg::CG;
 
@@ -583,6 +622,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     prefetch_tmap(&tm_values);
     prefetch_tmap(&tm_b);
     if constexpr (Cfg::PRE) prefetch_tmap(&tm_e);
+    if (!kCT && p.tma_c) prefetch_tmap(&tm_c);
   }
   if (warp == Cfg::W_MMA) {
     if constexpr (CG == 2) tmem_alloc_2sm<512>(smem_u32(tmem_base_slot));
@@ -738,7 +778,8 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
-    else epilogue_role<Cfg, kBF16, CG, kCT, kGELU>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
+    else epilogue_role<Cfg, kBF16, CG, kCT, kGELU>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot,
+                                                   (!kCT && p.tma_c) ? &tm_c : nullptr);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high

@@ -66,7 +66,7 @@ venom_status_t launch_cg(Kern kern, int cg, int grid, int threads, int smem, cud
 // ------------------------------------------------------------------ gathered / contiguous kernel
 template <class Cfg, bool kBF16>
 venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUtensorMap& te,
-                        SpmmParams p, int max_ctas, cudaStream_t s) {
+                        const CUtensorMap& tc, SpmmParams p, int max_ctas, cudaStream_t s) {
   // token-major C is a separate instantiation: a runtime branch in the epilogue cost the row-major
   // kernels up to 12% (measured on BERT FFN1)
   auto kern = p.c_t ? (p.M == 4 ? vnm_spmm_kernel<Cfg, kBF16, true, true>
@@ -102,35 +102,36 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUte
   // measured slower there (2.16 vs 2.01 ms): the gathers of B are the latency-critical stream, and
   // the T-band order keeps the fewest B column slabs live in L2
   if (p.group_n <= 0) p.group_n = 1;
-  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, te, p);
+  if (Cfg::MB != 1) p.tma_c = 0;  // the two-accumulator epilogue stores directly
+  return launch_cg(kern, Cfg::CG, grid, Cfg::NUM_THREADS, smem, s, tv, tb, te, tc, p);
 }
 
 // Gathered / contiguous kernel configurations. PRE: metadata pre-ordered for the tensor core.
 template <bool PRE, bool kBF16>
 venom_status_t run_gather(int NBg, int pair, int tile_t, const CUtensorMap& tv, const CUtensorMap& tb,
-                          const CUtensorMap& te, SpmmParams p, int max_ctas, cudaStream_t s) {
+                          const CUtensorMap& te, const CUtensorMap& tc, SpmmParams p, int max_ctas, cudaStream_t s) {
   if constexpr (PRE) {
     // two 128-row blocks per CTA of a pair (512 × 240 pair tiles): 1.45× fewer landed bytes per
     // useful FLOP than 256 × 256 pair tiles, for the contiguous (M = 4) operand
     if (tile_t == 240 && NBg == 1 && pair == 2 && p.M == 4)
-      return run_spmm<SpmmCfg<1, 240, 3, 4, 2, true, 2>, kBF16>(tv, tb, te, p, max_ctas, s);
+      return run_spmm<SpmmCfg<1, 240, 3, 4, 2, true, 2>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   }
   if (NBg == 1 && pair == 2) {
-    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 4, 8, 2, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 6, 8, 2, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
+    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 4, 8, 2, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 6, 8, 2, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else if (NBg == 1) {
     // 11 gather-issuing warps: TMA instructions issue serially within a warp, and a stage's 128
     // gather4 ops spread over 12-15 warps land ~1.1-1.15x faster than over 8
     // (tools/microbench_feed.cu); 20 warps in all keep 96 registers per thread (21 would cap at 80)
-    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 2, VENOM_GATHER_P, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
-    if (tile_t == 192) return run_spmm<SpmmCfg<1, 192, 3, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
-    if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 4, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm<SpmmCfg<1, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
+    if (tile_t == 256) return run_spmm<SpmmCfg<1, 256, 2, VENOM_GATHER_P, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 192) return run_spmm<SpmmCfg<1, 192, 3, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm<SpmmCfg<1, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else if (NBg == 2) {
-    if (tile_t == 128) return run_spmm<SpmmCfg<2, 128, 2, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
-    if (tile_t == 64) return run_spmm<SpmmCfg<2, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
+    if (tile_t == 128) return run_spmm<SpmmCfg<2, 128, 2, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm<SpmmCfg<2, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else {
-    if (tile_t == 64) return run_spmm<SpmmCfg<4, 64, 2, 8, 1, PRE>, kBF16>(tv, tb, te, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm<SpmmCfg<4, 64, 2, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   }
   return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
 }
@@ -193,7 +194,7 @@ venom_status_t run_densek_cfg(int M, int pair, int tile_t, const CUtensorMap& tb
 // ------------------------------------------------------------------ launchers (one per unit)
 #define VENOM_GATHER_ARGS                                                                       \
   int NBg, int pair, int tile_t, const CUtensorMap &tv, const CUtensorMap &tb, const CUtensorMap &te, \
-      SpmmParams p, int max_ctas, cudaStream_t s
+      const CUtensorMap &tc, SpmmParams p, int max_ctas, cudaStream_t s
 #define VENOM_DENSEK_ARGS \
   int M, int pair, int tile_t, const CUtensorMap &tb, EncodeTiledFn enc, SpmmParams p, int max_ctas, cudaStream_t s
 

@@ -3,6 +3,6 @@
 
 namespace venom {
 namespace launch {
-venom_status_t gather_pre_bf16(VENOM_GATHER_ARGS) { return run_gather<true,true>(NBg, pair, tile_t, tv, tb, te, p, max_ctas, s); }
+venom_status_t gather_pre_bf16(VENOM_GATHER_ARGS) { return run_gather<true,true>(NBg, pair, tile_t, tv, tb, te, tc, p, max_ctas, s); }
 }  // namespace launch
 }  // namespace venom

@@ -515,6 +515,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.c_t = ct ? 1 : 0;
   p.bk = bk ? 1 : 0;
   p.act = act;
+  p.tma_c = 0;
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -609,10 +610,26 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   } else if (!p.b3d && !encode_b(&tb, contiguous ? 128 : 1)) {
     return VENOM_ERR_CUDA;
   }
+  // C: row-major output through TMA boxes of 32 rows × 32 columns (64-byte swizzle, the epilogue's
+  // staging layout); token-major C keeps its direct stores
+  CUtensorMap tc = tv;
+  p.tma_c = 0;
+  if (!ct) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(R)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldc)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+        CUDA_SUCCESS)
+      p.tma_c = 1;
+    else
+      tc = tv;
+  }
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
   if (meta_tc == nullptr)
-    return bf16 ? venom::launch::gather_nopre_bf16(NBg, pair, tile_t, tv, tb, tv, p, max_ctas, s)
-                : venom::launch::gather_nopre_f16(NBg, pair, tile_t, tv, tb, tv, p, max_ctas, s);
+    return bf16 ? venom::launch::gather_nopre_bf16(NBg, pair, tile_t, tv, tb, tv, tc, p, max_ctas, s)
+                : venom::launch::gather_nopre_f16(NBg, pair, tile_t, tv, tb, tv, tc, p, max_ctas, s);
   // pre-ordered metadata: the [tiles·num_ks] contiguous 2 KB stage blocks, mapped as 2-D
   // [blocks][256] u64 with a one-row box, so each block is one 2 KB TMA row (a 16-byte-wide box of
   // 128 rows would cost the TMA unit 128 row requests per stage)
@@ -629,8 +646,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return VENOM_ERR_CUDA;
   }
-  return bf16 ? venom::launch::gather_pre_bf16(NBg, pair, tile_t, tv, tb, te, p, max_ctas, s)
-              : venom::launch::gather_pre_f16(NBg, pair, tile_t, tv, tb, te, p, max_ctas, s);
+  return bf16 ? venom::launch::gather_pre_bf16(NBg, pair, tile_t, tv, tb, te, tc, p, max_ctas, s)
+              : venom::launch::gather_pre_f16(NBg, pair, tile_t, tv, tb, te, tc, p, max_ctas, s);
 }
 
 int64_t venom_metadata_tc_bytes(int64_t R, int64_t K, venom_format_t f) {
