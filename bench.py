@@ -443,26 +443,41 @@ def run_gpu(args, ws, rank, local):
         del dense
     speedup = [c / s for c, s in zip(cub, per_launch_ms)]
 
-    # the optional tensor-parallel all-gather of C (tp.py), timed separately (N > 1, strong)
+    # the optional tensor-parallel all-gather of C (tp.py), timed separately (N > 1, strong): the
+    # token-major SpMM followed by NCCL all_gather_into_tensor, and the fused variant whose epilogue
+    # stores the slice into every rank's symmetric-memory buffer (opts.c_peers) + a barrier
     allgather = None
     if ws > 1 and args.scaling == "strong":
         from paper_2310_02065_b200 import tp
         L = layers[0]
         c_tm = venom.spmm(L.y, L.B, bias=L.bias, transposed_out=True)
         full_tm = torch.empty((L.T * ws, L.w["R"]), dtype=c_tm.dtype, device=device)
-        for _ in range(3):
-            tp.gather_token_major(c_tm, out=full_tm)
-        torch.cuda.synchronize(device)
-        barrier(ws)
-        a, b = ev_pair()
-        a.record(stream)
-        for _ in range(10):
-            tp.gather_token_major(c_tm, out=full_tm)
-        b.record(stream)
-        torch.cuda.synchronize(device)
-        ag_ms = max_over_ranks(a.elapsed_time(b) / 10, ws, device)
-        allgather = {"ms": round(ag_ms, 4), "bytes_received_per_rank": int(c_tm.numel() * 2 * (ws - 1)),
-                     "what": "NCCL all_gather_into_tensor of the token-major C slices (tp.py), not in value"}
+
+        def timed(fn, n=10):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize(device)
+            barrier(ws)
+            a, b = ev_pair()
+            a.record(stream)
+            for _ in range(n):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize(device)
+            return max_over_ranks(a.elapsed_time(b) / n, ws, device)
+
+        ag_ms = timed(lambda: tp.gather_token_major(c_tm, out=full_tm))
+        unfused_ms = timed(lambda: tp.spmm_tp_allgather(L.y, L.B, bias=L.bias, out=full_tm))
+        allgather = {"allgather_ms": round(ag_ms, 4), "spmm_then_allgather_ms": round(unfused_ms, 4),
+                     "bytes_received_per_rank": int(c_tm.numel() * 2 * (ws - 1)),
+                     "what": "tensor-parallel all-gather of C (tp.py), not in value"}
+        try:
+            buf, hdl = tp.fused_allgather_buffer(L.w["R"], L.T * ws, torch.float16, device)
+            fused_ms = timed(lambda: tp.spmm_tp_fused_allgather(L.y, L.B, buf, hdl, bias=L.bias))
+            ok = bool(torch.equal(buf, full_tm))
+            allgather.update({"spmm_fused_allgather_ms": round(fused_ms, 4), "fused_equals_nccl": ok})
+        except Exception as e:  # symmetric memory unavailable
+            allgather["fused"] = f"unavailable: {e!r}"[:200]
 
     # e2e through the public API with pinned host buffers
     e2e = None

@@ -240,6 +240,15 @@ typedef struct {
   int32_t group_n;     /* tile order: column tiles are taken in groups of group_n, the row tiles
                         outer within a group (1 = all row tiles of one column band first). 0: the
                         library default (1). */
+  void* const* c_peers;  /* fused all-gather: host array of n_peers
+                        DEVICE pointers (e.g. the other ranks' full output buffers mapped peer-to-peer,
+                        each already offset to where this rank's slice starts; 16-byte aligned, same
+                        ldc as C). Every element of C is also stored there by the epilogue, so the
+                        SpMM's output lands in all ranks' buffers without a separate collective. The
+                        caller orders the ranks' kernels with the consumers (e.g. a barrier). Gathered
+                        / contiguous kernel, one accumulator per CTA (dense-K and tile_t 240 return
+                        VENOM_ERR_INVALID_ARGUMENT). NULL / 0: none. */
+  int32_t n_peers;     /* 0..8 */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

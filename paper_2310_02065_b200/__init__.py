@@ -52,7 +52,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("tile_t", ctypes.c_int32), ("stages", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
                 ("metadata_tc", ctypes.c_void_p), ("c_transposed", ctypes.c_int32),
-                ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32), ("group_n", ctypes.c_int32)]
+                ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32), ("group_n", ctypes.c_int32),
+                ("c_peers", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_int32)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -285,14 +286,16 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
          max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0,
          use_metadata_tc: bool = True, transposed_out: bool = False,
-         b_kmajor: bool = False, gelu: bool = False, group_n: int = 0) -> torch.Tensor:
+         b_kmajor: bool = False, gelu: bool = False, group_n: int = 0,
+         c_peers=None) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T], or with
     ``transposed_out`` the token-major C^T: dtype[T, R] (row stride may exceed R). When x carries
     tensor-core-ordered metadata (order_metadata) it is used unless use_metadata_tc is False.
     ``b_kmajor``: B is token-major dtype[T, K] (M = 4 operands); with ``transposed_out`` this is
     ``F.linear(B, decompress(x))`` on PyTorch-layout activations. ``gelu``: GELU after the bias in
-    the epilogue (row-major B and C)."""
+    the epilogue (row-major B and C). ``c_peers``: the fused all-gather — device addresses (or
+    tensors) where the epilogue also stores C, same layout and leading dimension (tp.py)."""
     assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[1 if b_kmajor else 0] == x.K
     assert B.dtype == x.dtype
     T = B.shape[0 if b_kmajor else 1]
@@ -303,8 +306,15 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     if bias is not None:
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
     mtc = x.metadata_tc.data_ptr() if (use_metadata_tc and x.metadata_tc is not None) else None
+    peers = None
+    if c_peers:
+        # fused all-gather: device addresses (ints or tensors) of the peer output slices
+        addrs = [p if isinstance(p, int) else p.data_ptr() for p in c_peers]
+        peers = (ctypes.c_void_p * len(addrs))(*addrs)
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
-                 1 if b_kmajor else 0, 1 if gelu else 0, group_n)
+                 1 if b_kmajor else 0, 1 if gelu else 0, group_n,
+                 ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p)) if peers is not None else None,
+                 len(c_peers) if c_peers else 0)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
                              ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
                              ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),

@@ -33,6 +33,8 @@
 
 namespace venom {
 
+constexpr int kMaxPeers = 8;  // fused all-gather fan-out (one 8-GPU NVSwitch node)
+
 struct SpmmParams {
   const uint16_t* values;   // read directly by the dense-K expanders (the gathered kernel uses TMA)
   const uint8_t* metadata;
@@ -53,6 +55,11 @@ struct SpmmParams {
   int bk;   // B given K-major (token-major activations, dtype[T][ldb]); M = 4 operand only
   int act;  // 1: GELU after the bias (row-major C only)
   int tma_c;  // row-major C stored by TMA boxes (tm_c encoded by the host)
+  // fused all-gather: every C element is also stored at the same offset
+  // relative to each of n_peers other buffers (e.g. the other ranks' full-output buffers, mapped
+  // peer-to-peer over NVLink, each pointer already offset to this rank's slice)
+  int n_peers;
+  uint16_t* c_peers[kMaxPeers];
   int dbg;  // debug/ablation flags (0 in production)
 };
 
@@ -334,9 +341,13 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
           const int jj = 32 * c + 2 * j + (odd ? 1 : 0);  // column within the warp's slice
           const int64_t t = col_base + jj;
           if (jj < HC && t < p.T && r0 < p.R) {
-            uint16_t* dst = p.C + t * p.ldc + r0;
-            if (r0 + 1 < p.R) *reinterpret_cast<uint32_t*>(dst) = v;
-            else *dst = static_cast<uint16_t>(v & 0xFFFFu);
+            const int64_t off = t * p.ldc + r0;
+            const bool pair = r0 + 1 < p.R;
+            for (int pp = -1; pp < p.n_peers; ++pp) {  // this rank's C, then the fused all-gather
+              uint16_t* dst = (pp < 0 ? p.C : p.c_peers[pp]) + off;
+              if (pair) *reinterpret_cast<uint32_t*>(dst) = v;
+              else *dst = static_cast<uint16_t>(v & 0xFFFFu);
+            }
           }
         }
     } else if (p.dbg & 4) {  // ablation 4: no C stores
@@ -368,6 +379,23 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
         if (lane == 0) {
           tma_store_2d(tm_c, slot, static_cast<int32_t>(col_base + 32 * c), row_base);
           bulk_commit_group();
+        }
+        if (p.n_peers > 0) {
+          // fused all-gather: the same chunk from the slot to every peer buffer, 8 rows × 64
+          // contiguous bytes per store instruction (the slot stays valid: it is rewritten only
+          // after this warp's next pass)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), sgm = lane & 3;
+            uint4 o;
+            const uint32_t a = slot + r * 64 + ((sgm ^ ((r >> 1) & 3)) * 16);
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
+            const int64_t orow = row_base + r;
+            const int64_t ocol = col_base + 32 * c + 8 * sgm;
+            if (orow < p.R && ocol < p.T)
+              for (int pp = 0; pp < p.n_peers; ++pp)
+                *reinterpret_cast<uint4*>(p.c_peers[pp] + orow * p.ldc + ocol) = o;
+          }
         }
       }
       if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(10, tl);

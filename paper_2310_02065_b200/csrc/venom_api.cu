@@ -491,6 +491,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   else if (!can_gather) use_densek = true;
   else if (!can_densek) use_densek = false;
   else use_densek = false;  // measured: the gathered / contiguous kernel wins wherever it applies
+  if (opts && opts->n_peers != 0 && use_densek) return VENOM_ERR_INVALID_ARGUMENT;  // no fan-out in dense-K
 
   SpmmParams p;
   p.values = static_cast<const uint16_t*>(values);
@@ -516,6 +517,20 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.bk = bk ? 1 : 0;
   p.act = act;
   p.tma_c = 0;
+  p.n_peers = 0;
+  for (int i = 0; i < venom::kMaxPeers; ++i) p.c_peers[i] = nullptr;
+  if (opts && opts->n_peers != 0) {
+    // fused all-gather: peer output buffers (row-major C through the TMA-store epilogue, or
+    // token-major C); each 16-byte aligned, addressed like C (same ldc)
+    if (opts->n_peers < 0 || opts->n_peers > venom::kMaxPeers || !opts->c_peers || strategy == VENOM_STRATEGY_DENSE_K ||
+        (opts->tile_t == 240))
+      return VENOM_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < opts->n_peers; ++i) {
+      if (!opts->c_peers[i] || !aligned(opts->c_peers[i], 16)) return VENOM_ERR_INVALID_ARGUMENT;
+      p.c_peers[i] = static_cast<uint16_t*>(opts->c_peers[i]);
+    }
+    p.n_peers = opts->n_peers;
+  }
   p.dbg = debug_flags();
   auto set_tiles = [&](int bn) {
     p.n_tiles = static_cast<int>((T + bn - 1) / bn);
@@ -626,6 +641,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     else
       tc = tv;
   }
+  if (p.n_peers > 0 && !ct && !p.tma_c) return VENOM_ERR_INVALID_ARGUMENT;
   const uint8_t* meta_tc = opts ? opts->metadata_tc : nullptr;
   if (meta_tc == nullptr)
     return bf16 ? venom::launch::gather_nopre_bf16(NBg, pair, tile_t, tv, tb, tv, tc, p, max_ctas, s)

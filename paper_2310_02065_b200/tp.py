@@ -47,3 +47,36 @@ def spmm_tp_allgather(x, B_local: torch.Tensor, bias: Optional[torch.Tensor] = N
     from . import spmm
     c_local = spmm(x, B_local, bias=bias, transposed_out=True, **kw)
     return gather_token_major(c_local, out=out, group=group)
+
+
+# ------------------------------------------------------------------ fused all-gather (§8(f) rank 3)
+def fused_allgather_buffer(R: int, T: int, dtype, device, group=None):
+    """The full token-major output C^T [T, R] on every rank, in symmetric memory (peer-mapped over
+    NVLink / NVSwitch), and its rendezvous handle (the peers' buffer addresses and a barrier)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    buf = symm_mem.empty((T, R), dtype=dtype, device=device)
+    hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+    return buf, hdl
+
+
+def peer_slices(hdl, t0: int, R: int, elem_size: int, rank: int):
+    """Addresses where this rank's token rows [t0, ...) start in every OTHER rank's full buffer."""
+    return [int(p) + t0 * R * elem_size for r, p in enumerate(hdl.buffer_ptrs) if r != rank]
+
+
+def spmm_tp_fused_allgather(x, B_local: torch.Tensor, buf: torch.Tensor, hdl, bias=None, group=None, **kw):
+    """The T-split SpMM with the all-gather fused into its epilogue: this rank's slice of C^T is
+    stored into its own full buffer AND, by the same kernel, into every peer's buffer (peer-to-peer
+    stores over NVLink, no separate collective; include/venom.h opts.c_peers). A barrier on the
+    symmetric-memory handle then orders every rank's stores before the buffer is read.
+    B_local: this rank's [K, T/world] column slice of the global B."""
+    from . import spmm
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    T, R = buf.shape
+    t0, t1 = t_slice(T, world, rank)
+    assert B_local.shape[1] == t1 - t0
+    spmm(x, B_local, bias=bias, out=buf[t0:t1], transposed_out=True,
+         c_peers=peer_slices(hdl, t0, R, buf.element_size(), rank), **kw)
+    hdl.barrier(channel=0)
+    return buf

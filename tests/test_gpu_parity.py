@@ -955,3 +955,78 @@ def test_compress_out_refreshes_tensor_core_metadata():
     C = venom.spmm(x, to_dev(B, F16))  # uses x.metadata_tc
     parts = oracle.compress(A2, F16, V=V, M=M)
     check_spmm(C, oracle.spmm(*parts, R, K, F16, V, M, B), F16)
+
+
+@pytest.mark.parametrize("R,K,T,dt", [(256, 512, 128, F16), (1024, 4096, 512, F16), (512, 1024, 256, BF16)])
+def test_spmm_m4_matches_cusparselt(R, K, T, dt):
+    """SURVEY §8(c) M = 4 pin: plain 2:4 magnitude pruning (V:2:4) multiplied by cuSPARSELt
+    (torch._cslt_sparse_mm on the same pruned weight, a library routine) agrees with venom_spmm
+    within the north-star tolerance, and both with the oracle."""
+    if not torch.backends.cusparselt.is_available():
+        pytest.skip("cuSPARSELt not available in this torch build")
+    A, B, _, parts = oracle_problem(R, K, T, 128, 4, dt, 61 + R + K, False)
+    x = venom.order_metadata(vnm_from(parts, R, K, 128, 4, dt))
+    Ap = venom.decompress(x)
+    Bd = to_dev(B, dt)
+    C_lt = torch._cslt_sparse_mm(torch._cslt_compress(Ap), Bd)
+    C_v = venom.spmm(x, Bd)
+    C_ref = oracle.spmm(*parts, R, K, dt, 128, 4, B)
+    check_spmm(C_v, C_ref, dt)
+    got_lt = C_lt.double().cpu().numpy()
+    assert rel_fro(bits_to_f64(to_bits(C_v), dt), got_lt) <= TOL_FRO
+
+
+def test_spmm_fused_allgather_fanout():
+    """The fused all-gather's epilogue fan-out (opts.c_peers), on one GPU: peer buffers that are
+    other allocations on this device must receive exactly this call's C — row-major C (TMA-store
+    epilogue + copies from the staging slot) and token-major C, ragged edges included."""
+    for (R, K, T, V, M, ct) in [(256, 512, 136, 128, 16, False), (192, 512, 256, 64, 8, True),
+                                (256, 1024, 264, 128, 4, False), (384, 512, 200, 128, 16, True)]:
+        A, B, bv, parts = oracle_problem(R, K, T, V, M, F16, 91 + R + T, True)
+        x = venom.order_metadata(vnm_from(parts, R, K, V, M, F16))
+        Bd, bd = to_dev(B, F16), to_dev(bv, F16)
+        shape = (T, R) if ct else (R, T)
+        peers = [torch.full(shape, float("nan"), dtype=torch.float16, device=Bd.device) for _ in range(3)]
+        C = venom.spmm(x, Bd, bias=bd, transposed_out=ct, c_peers=peers)
+        torch.cuda.synchronize()
+        for q in peers:
+            assert torch.equal(q, C)
+        C_ref = oracle.spmm(*parts, R, K, F16, V, M, B, bias=bv)
+        check_spmm(C.t() if ct else C, C_ref, F16)
+    with pytest.raises(venom.VenomError):
+        venom.spmm(x, Bd, c_peers=[peers[0]] * 9)
+    with pytest.raises(venom.VenomError):
+        venom.spmm(vnm_from(parts, R, K, V, M, F16), Bd, strategy=venom.STRATEGY_DENSE_K, c_peers=[peers[0]])
+
+
+def test_tensor_parallel_fused_allgather_on_gpu():
+    """tp.spmm_tp_fused_allgather over symmetric memory on a one-rank NCCL group: the full C^T in
+    the symmetric buffer equals venom.spmm's C transposed (the peer fan-out itself is covered by
+    test_spmm_fused_allgather_fanout; more ranks need more GPUs than this run has)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2310_02065_b200 import tp
+    R, K, T, V, M = 256, 512, 256, 128, 16
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, F16, 79, True)
+    x = venom.order_metadata(vnm_from(parts, R, K, V, M, F16))
+    created = False
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                                device_id=torch.device("cuda", 0))
+        created = True
+    try:
+        Bd, bd = to_dev(B, F16), to_dev(bv, F16)
+        try:
+            buf, hdl = tp.fused_allgather_buffer(R, T, torch.float16, Bd.device)
+        except Exception as e:  # symmetric memory unavailable in this build / environment
+            pytest.skip(f"symmetric memory unavailable: {e!r}")
+        t0, t1 = tp.t_slice(T, dist.get_world_size(), dist.get_rank())
+        tp.spmm_tp_fused_allgather(x, Bd[:, t0:t1], buf, hdl, bias=bd)
+        torch.cuda.synchronize()
+        assert torch.equal(buf.t(), venom.spmm(x, Bd, bias=bd))
+    finally:
+        if created:
+            dist.destroy_process_group()

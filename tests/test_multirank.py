@@ -89,6 +89,12 @@ def _worker(rank: int, ws: int, port: int, q):
             assert np.array_equal(full_tm.numpy(), oracle.spmm(*parts, R, K, synth.F16, V, M, B).T)
         with pytest.raises(ValueError):
             tp.t_slice(100, ws, rank)
+        # fused all-gather addressing: this rank's slice [t0, t1) of C^T [T, R] lands at row t0 of
+        # every OTHER rank's buffer (host arithmetic of tp.peer_slices)
+        class _H:
+            buffer_ptrs = [1 << 40, 2 << 40, 3 << 40][:ws]
+        ps = tp.peer_slices(_H, t0, R, 2, rank)
+        assert ps == [b + t0 * R * 2 for r, b in enumerate(_H.buffer_ptrs) if r != rank] and len(ps) == ws - 1
 
         # weak scaling draws per-rank activations: the ranks' B differ
         b_r = torch.from_numpy(synth.gaussian((8, 8), 1.0, synth.F16, 1001 + 7919 * rank).astype(np.int32))
