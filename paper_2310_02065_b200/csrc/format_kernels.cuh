@@ -272,18 +272,24 @@ struct TileView {
 // Phases 1-4 of the compressor on one V × W tile already in shared memory (`tile`, pitch W); the
 // scratch arrays live at `smem_raw` + CompressTileLayout offsets. Called by the tile kernel (after
 // its own loads) and by the persistent TMA kernel (once per tile of its pipeline).
-template <bool kBF16, bool kExpand>
+// MC / GPC / NTHR: compile-time M, groups per tile and block size (0 = runtime). With all three
+// fixed and G % GPC == 0 (every tile full), the per-tile index arithmetic has no divisions — round 2
+// measured the per-tile setup at a third of the compressor's instructions, mostly divisions by
+// runtime M and group counts.
+template <bool kBF16, bool kExpand, int MC = 0, int GPC = 0, int NTHR = 0>
 __device__ __forceinline__ void compress_tile_process(
-    const TileView tile, uint8_t* smem_raw, int64_t R, int64_t K, int V, int M, int64_t G,
-    int gpc, int64_t rb, int64_t g0, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
+    const TileView tile, uint8_t* smem_raw, int64_t R, int64_t K, int V, int M_in, int64_t G,
+    int gpc_in, int64_t rb, int64_t g0, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
     uint8_t* __restrict__ column_idx, int32_t* __restrict__ status, uint32_t* __restrict__ values2,
     uint32_t* __restrict__ meta_tc, int dbg, int nbuf) {
-  const int ng = static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
+  const int M = MC ? MC : M_in;
+  const int gpc = GPC ? GPC : gpc_in;
+  const int ng = GPC ? GPC : static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
   const int W = gpc * M;                 // tile pitch (elements)
   const int ncols = ng * M;
   const int64_t row0 = rb * V;
   const int64_t meta_row = (G + 1) / 2;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x, nthr = NTHR ? NTHR : static_cast<int>(blockDim.x);
   constexpr int NS = CompressTileLayout::NS;
   const CompressTileLayout lay(V, W, gpc, kExpand, nbuf, tile.swz);  // scratch after the nbuf tile buffers
   float* s_part = reinterpret_cast<float*>(smem_raw + lay.part);       // [NS][W]
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(512) vnm_compress_tile_kernel(
 // mbarrier-completed) while phases 1-4 run on the current one, so HBM streams continuously and
 // the per-CTA prologue is paid once (the one-tile-per-CTA kernel spent its time in load latency,
 // prologue and barriers: 0.61 ms for the GPT-3 FFN weight).
-template <bool kBF16, bool kExpand>
+template <bool kBF16, bool kExpand, int MC = 0, int GPC = 0>
 __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
     const __grid_constant__ CUtensorMap tm_a, int64_t R, int64_t K, int V, int M, int64_t G, int gpc,
     int64_t nchunks, int64_t ntiles, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
@@ -747,7 +753,8 @@ __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
     const int b = it & 1;
     mbar_wait(smem_u32(&full[b]), (it >> 1) & 1);
     const int64_t rb = t / nchunks, cc = t - rb * nchunks;
-    compress_tile_process<kBF16, kExpand>(TileView{reinterpret_cast<const uint16_t*>(smem_raw + b * lay.tile_bytes), 0,
+    compress_tile_process<kBF16, kExpand, MC, GPC, (MC && GPC) ? 256 : 0>(
+        TileView{reinterpret_cast<const uint16_t*>(smem_raw + b * lay.tile_bytes), 0,
                                                    static_cast<int>(box_stride / 2), true}, smem_raw,
                                           R, K, V, M, G, gpc, rb, cc * gpc, values, metadata, column_idx, status,
                                           values2, meta_tc, dbg, 2);

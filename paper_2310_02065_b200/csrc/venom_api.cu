@@ -183,6 +183,17 @@ venom_status_t venom_compress(const void* A, int64_t R, int64_t K, int64_t lda, 
     if (tsmem <= 100 * 1024 && tma_compress_ok(A, lda, f.v, gt * f.m)) {
       auto kern = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, false>
                                      : venom::vnm_compress_tma_kernel<false, false>;
+      // compile-time shapes (no per-tile divisions) for the configurations the benchmarks run
+      const bool full = G % gt == 0;
+      if (full && f.m == 16 && gt == 8)
+        kern = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, false, 16, 8>
+                                  : venom::vnm_compress_tma_kernel<false, false, 16, 8>;
+      else if (full && f.m == 8 && gt == 32)
+        kern = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, false, 8, 32>
+                                  : venom::vnm_compress_tma_kernel<false, false, 8, 32>;
+      else if (full && f.m == 32 && gt == 4)
+        kern = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, false, 32, 4>
+                                  : venom::vnm_compress_tma_kernel<false, false, 32, 4>;
       return launch_compress_tma(kern, A, R, K, lda, f, gt, false, values, metadata, column_idx, dev_status,
                                  nullptr, nullptr, s);
     }
@@ -266,6 +277,12 @@ venom_status_t venom_compress_2to4(const void* A, int64_t R, int64_t K, int64_t 
   if (tma_compress_ok(A, lda, f.v, W) && !(debug_flags() & 32)) {
     auto kt = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, true>
                                  : venom::vnm_compress_tma_kernel<false, true>;
+    if (G % gt == 0 && f.m == 8 && gt == 32)
+      kt = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, true, 8, 32>
+                              : venom::vnm_compress_tma_kernel<false, true, 8, 32>;
+    else if (G % gt == 0 && f.m == 16 && gt == 16)
+      kt = (dt == VENOM_BF16) ? venom::vnm_compress_tma_kernel<true, true, 16, 16>
+                              : venom::vnm_compress_tma_kernel<false, true, 16, 16>;
     return launch_compress_tma(kt, A, R, K, lda, f, gt, true, values, metadata, column_idx, dev_status,
                                static_cast<uint32_t*>(values_2to4), reinterpret_cast<uint32_t*>(metadata_2to4_tc),
                                static_cast<cudaStream_t>(stream));
