@@ -278,10 +278,17 @@ struct TileView {
 // runtime M and group counts.
 template <bool kBF16, bool kExpand, int MC = 0, int GPC = 0, int NTHR = 0>
 __device__ __forceinline__ void compress_tile_process(
-    const TileView tile, uint8_t* smem_raw, int64_t R, int64_t K, int V, int M_in, int64_t G,
+    const TileView tile_in, uint8_t* smem_in, int64_t R, int64_t K, int V, int M_in, int64_t G,
     int gpc_in, int64_t rb, int64_t g0, uint16_t* __restrict__ values, uint8_t* __restrict__ metadata,
     uint8_t* __restrict__ column_idx, int32_t* __restrict__ status, uint32_t* __restrict__ values2,
     uint32_t* __restrict__ meta_tc, int dbg, int nbuf) {
+  // the tile and scratch pointers re-derived from the dynamic shared-memory symbol: the compiler
+  // then emits shared-space accesses (LDS / STS, 32-bit addresses) instead of generic ones (ncu
+  // showed LD.E / ST.E with 64-bit address arithmetic when they arrived as plain pointers)
+  extern __shared__ __align__(16) uint8_t smem_dyn[];
+  uint8_t* smem_raw = smem_dyn + (smem_in - smem_dyn);
+  TileView tile = tile_in;
+  tile.base = reinterpret_cast<const uint16_t*>(smem_dyn + (reinterpret_cast<const uint8_t*>(tile_in.base) - smem_dyn));
   const int M = MC ? MC : M_in;
   const int gpc = GPC ? GPC : gpc_in;
   const int ng = GPC ? GPC : static_cast<int>((G - g0) < gpc ? (G - g0) : gpc);  // groups in this chunk
@@ -290,6 +297,7 @@ __device__ __forceinline__ void compress_tile_process(
   const int64_t row0 = rb * V;
   const int64_t meta_row = (G + 1) / 2;
   const int tid = threadIdx.x, nthr = NTHR ? NTHR : static_cast<int>(blockDim.x);
+
   constexpr int NS = CompressTileLayout::NS;
   const CompressTileLayout lay(V, W, gpc, kExpand, nbuf, tile.swz);  // scratch after the nbuf tile buffers
   float* s_part = reinterpret_cast<float*>(smem_raw + lay.part);       // [NS][W]
