@@ -850,13 +850,16 @@ __global__ void __launch_bounds__(256) vnm_decompress_m8_kernel(
     const uint32_t* __restrict__ values, const uint8_t* __restrict__ metadata,
     const uint32_t* __restrict__ column_idx, int R, int K, int V, int M, int G,
     uint16_t* __restrict__ out, int64_t lda, int32_t* __restrict__ status) {
-  const int chunks = K / 8;
-  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
-  if (ch >= chunks) return;
-  const int meta_row = (G + 1) / 2;
+  // thread per (group, ROWS rows) when CPG is a compile-time 1 / 2 / 4: one set of loads (value
+  // pair, nibble, column word) per row fills the group's whole M outputs (CPG 16-byte stores);
+  // CPG = 0 (runtime M): thread per 8-output chunk
+  constexpr int NCH = CPG ? CPG : 1;
   const int cpg = CPG ? CPG : M / 8;  // 8-output chunks per group
-  const int g = ch / cpg;
-  const int j0 = (ch - g * cpg) * 8;  // first column of this chunk within the group
+  const int unit = blockIdx.x * blockDim.x + threadIdx.x;  // group (CPG) or chunk (runtime M)
+  const int g = CPG ? unit : unit / cpg;
+  if (CPG ? (unit >= G) : (unit >= K / 8)) return;
+  const int jbase = CPG ? 0 : (unit - g * cpg) * 8;  // first column of this thread's chunk(s) in the group
+  const int meta_row = (G + 1) / 2;
   const bool same_block = (V % ROWS) == 0;  // the ROWS rows of a slot share column_idx
   const bool check = status != nullptr;
   bool bad = false;
@@ -886,19 +889,22 @@ __global__ void __launch_bounds__(256) vnm_decompress_m8_kernel(
         bad |= !((c & 0xFFu) < ((c >> 8) & 0xFFu) && ((c >> 8) & 0xFFu) < ((c >> 16) & 0xFFu) &&
                  ((c >> 16) & 0xFFu) < (c >> 24) && (c >> 24) < static_cast<uint32_t>(M)) ||
                !(p0 < p1);
-      // offsets of the two kept columns inside this 8-column chunk (outside [0, 8): not here);
-      // each lands in the low or high 64-bit half by a shift — no per-position branches
-      const uint32_t d0 = ((c >> (8 * p0)) & 0xFFu) - static_cast<uint32_t>(j0);
-      const uint32_t d1 = ((c >> (8 * p1)) & 0xFFu) - static_cast<uint32_t>(j0);
+      const uint32_t c0 = (c >> (8 * p0)) & 0xFFu, c1 = (c >> (8 * p1)) & 0xFFu;  // kept columns in the group
       const uint64_t x0 = vv[u] & 0xFFFFu, x1 = vv[u] >> 16;
-      uint64_t lo = 0, hi = 0;
-      lo |= (d0 < 4u) ? (x0 << (16 * d0)) : 0ull;
-      hi |= (d0 - 4u < 4u) ? (x0 << (16 * (d0 - 4u))) : 0ull;
-      lo |= (d1 < 4u) ? (x1 << (16 * d1)) : 0ull;
-      hi |= (d1 - 4u < 4u) ? (x1 << (16 * (d1 - 4u))) : 0ull;
-      __stcs(reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * lda + 8 * ch),
-             make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32), static_cast<uint32_t>(hi),
-                        static_cast<uint32_t>(hi >> 32)));
+      uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(row) * lda + static_cast<int64_t>(g) * M + jbase);
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        // offsets of the two kept columns inside chunk k (outside [0, 8): not in it); each lands
+        // in the low or high 64-bit half by a shift — no per-position branches
+        const uint32_t d0 = c0 - static_cast<uint32_t>(jbase + 8 * k), d1 = c1 - static_cast<uint32_t>(jbase + 8 * k);
+        uint64_t lo = 0, hi = 0;
+        lo |= (d0 < 4u) ? (x0 << (16 * d0)) : 0ull;
+        hi |= (d0 - 4u < 4u) ? (x0 << (16 * (d0 - 4u))) : 0ull;
+        lo |= (d1 < 4u) ? (x1 << (16 * d1)) : 0ull;
+        hi |= (d1 - 4u < 4u) ? (x1 << (16 * (d1 - 4u))) : 0ull;
+        __stcs(dst + k, make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32), static_cast<uint32_t>(hi),
+                                   static_cast<uint32_t>(hi >> 32)));
+      }
     }
   }
   if (bad) atomicMax(status, kStatusCorruptMetadata);

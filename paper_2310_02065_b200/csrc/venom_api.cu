@@ -374,7 +374,8 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
   if (vec && f.m % 8 == 0 && R <= 0x7FFFFFFF) {
     constexpr int kRows = 4;  // rows per thread (loads of all of them in flight together)
     const int64_t slots = (R + kRows - 1) / kRows;
-    const dim3 g2(static_cast<unsigned>((K / 8 + 255) / 256), static_cast<unsigned>(slots < 65535 ? slots : 65535));
+    const int64_t units = (f.m == 8 || f.m == 16 || f.m == 32) ? G : K / 8;  // groups (compile-time M) or chunks
+    const dim3 g2(static_cast<unsigned>((units + 255) / 256), static_cast<unsigned>(slots < 65535 ? slots : 65535));
 #define VENOM_DEC8(C)                                                                                  \
   venom::vnm_decompress_m8_kernel<C, kRows><<<g2, 256, 0, s>>>(                                        \
       static_cast<const uint32_t*>(values), metadata, reinterpret_cast<const uint32_t*>(column_idx), \
