@@ -323,9 +323,11 @@ def ev_pair():
 
 def run_gpu(args, ws, rank, local):
     import paper_2310_02065_b200 as venom
-    device = torch.device("cuda", local)
+    # VENOM_BENCH_DEVICE / VENOM_BENCH_BACKEND: tools-only overrides that run several ranks on one
+    # GPU over gloo (the multi-rank code path checked on a one-GPU box; timings meaningless)
+    device = torch.device("cuda", int(os.environ.get("VENOM_BENCH_DEVICE", local)))
     torch.cuda.set_device(device)
-    init_dist(ws, "nccl")
+    init_dist(ws, os.environ.get("VENOM_BENCH_BACKEND", "nccl"))
     layers = [Layer(n, device, rank, ws, args.scaling, args.form) for n in WORKLOAD_SETS[args.workload]]
     kw = {}
     if args.tile_t:
@@ -466,11 +468,14 @@ def run_gpu(args, ws, rank, local):
             torch.cuda.synchronize(device)
             return max_over_ranks(a.elapsed_time(b) / n, ws, device)
 
-        ag_ms = timed(lambda: tp.gather_token_major(c_tm, out=full_tm))
-        unfused_ms = timed(lambda: tp.spmm_tp_allgather(L.y, L.B, bias=L.bias, out=full_tm))
-        allgather = {"allgather_ms": round(ag_ms, 4), "spmm_then_allgather_ms": round(unfused_ms, 4),
-                     "bytes_received_per_rank": int(c_tm.numel() * 2 * (ws - 1)),
+        allgather = {"bytes_received_per_rank": int(c_tm.numel() * 2 * (ws - 1)),
                      "what": "tensor-parallel all-gather of C (tp.py), not in value"}
+        try:
+            allgather["allgather_ms"] = round(timed(lambda: tp.gather_token_major(c_tm, out=full_tm)), 4)
+            allgather["spmm_then_allgather_ms"] = round(
+                timed(lambda: tp.spmm_tp_allgather(L.y, L.B, bias=L.bias, out=full_tm)), 4)
+        except Exception as e:  # e.g. a backend without all_gather_into_tensor on CUDA tensors
+            allgather["unfused"] = f"unavailable: {e!r}"[:200]
         try:
             buf, hdl = tp.fused_allgather_buffer(L.w["R"], L.T * ws, torch.float16, device)
             fused_ms = timed(lambda: tp.spmm_tp_fused_allgather(L.y, L.B, buf, hdl, bias=L.bias))
