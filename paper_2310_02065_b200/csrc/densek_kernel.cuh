@@ -31,6 +31,7 @@ namespace venom {
 template <int BN_, int STAGES_, int M_, int CG_ = 1>
 struct DenseKCfg {
   static constexpr int NB = 1;
+  static constexpr bool M64 = false;            // (shares spmm_kernel.cuh's epilogue)
   static constexpr int CG = CG_;                // 2: CTA pair (cta_group::2), M = 256 per MMA
   static constexpr int BN = BN_;
   static constexpr int STAGES = STAGES_;

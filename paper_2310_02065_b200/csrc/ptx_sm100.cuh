@@ -299,6 +299,15 @@ __device__ __forceinline__ void tma_prefetch_3d(const void* map, int32_t c0, int
                    reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// 4-D tiled load (c0 inner .. c3 outer)
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* map, uint32_t bar, int32_t c0,
+                                            int32_t c1, int32_t c2, int32_t c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+      : "memory");
+}
 // 3-D tiled load (c0 inner, c1, c2 outer)
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, uint32_t bar, int32_t c0,
                                             int32_t c1, int32_t c2, uint64_t policy) {

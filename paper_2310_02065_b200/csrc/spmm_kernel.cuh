@@ -44,6 +44,7 @@ struct SpmmParams {
   int64_t R, K, T, ldc;
   int V, M, G, meta_row;
   int num_ks;    // k-stages per tile: ceil(G / 32) gathered, ceil(K / 128) dense-K
+  int last_kb;   // gathered: K = 32 MMAs of the last k-stage that hold real groups (1..4)
   int m_tiles;   // ceil(R / 128)
   int n_tiles;   // ceil(T / BN)
   int num_tiles;
@@ -55,6 +56,7 @@ struct SpmmParams {
   int bk;   // B given K-major (token-major activations, dtype[T][ldb]); M = 4 operand only
   int act;  // 1: GELU after the bias (row-major C only)
   int tma_c;  // row-major C stored by TMA boxes (tm_c encoded by the host)
+  int e4d;    // M64 + pre-ordered metadata: tm_e is the 4-D lane-permuting map (else 8 row loads)
   // fused all-gather: every C element is also stored at the same offset
   // relative to each of n_peers other buffers (e.g. the other ranks' full-output buffers, mapped
   // peer-to-peer over NVLink, each pointer already offset to this rank's slice)
@@ -87,7 +89,13 @@ struct SpmmCfg {
   static constexpr int E_BYTES = PRE_ ? MB_ * E_BLOCK : 0;
   static constexpr int STAGE_BYTES = A_BYTES + NB * B_BYTES + E_BYTES;
   static constexpr int TX_BYTES = STAGE_BYTES;  // per CTA
-  static constexpr int ACC_COLS = NB * MB_ * BN;
+  // M64 (V = 64, two V-blocks per 128-row tile): each block is one M = 64 MMA on its own 64 A rows,
+  // its accumulator on one half of every TMEM lane quarter (block b: lanes 32q + 16b .. +15, the
+  // D and metadata addresses both offset by 16b lanes; probed in tools/probe_m64.cu). Both blocks
+  // share one BN-column accumulator: no wasted tensor work or TMEM, so the accumulator is
+  // double-buffered. V = 32 (NB = 4) keeps one M = 128 MMA per block into its own columns.
+  static constexpr bool M64 = (NB_ == 2);
+  static constexpr int ACC_COLS = (M64 ? 1 : NB) * MB_ * BN;
   // TMEM: accumulators, then 4 metadata columns per row block and stage
   static constexpr int E_PER_STAGE = 4 * MB_;
   static constexpr int ACC_BUFS = (2 * ACC_COLS + E_PER_STAGE * STAGES_ <= 512) ? 2 : 1;
@@ -192,7 +200,8 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
   using namespace ptx;
   constexpr int STAGES = Cfg::STAGES, NB = Cfg::NB, BN = Cfg::BN;
   // kBK: B' is K-major (bit 16 clear), else MN-major
-  constexpr uint32_t idesc = idesc_sp_f16(kBF16 ? 1u : 0u, 128 * CG, BN) & (kBK ? ~(1u << 16) : ~0u);
+  constexpr uint32_t idesc =
+      idesc_sp_f16(kBF16 ? 1u : 0u, Cfg::M64 ? 64 : 128 * CG, BN) & (kBK ? ~(1u << 16) : ~0u);
   for (int tl = 0; tl < my_tiles; ++tl) {
     const int ab = tl % Cfg::ACC_BUFS;
     const uint32_t aphase = (tl / Cfg::ACC_BUFS) & 1;
@@ -219,16 +228,23 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
             else tc_cp_128x128b(e_tmem + 4 * mb, edesc);
           }
         }
+        const int n_kb = (ks == p.num_ks - 1) ? p.last_kb : 4;
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
+          if (kb >= n_kb) break;
 #pragma unroll
           for (int b = 0; b < NB * Cfg::MB; ++b) {
             // MB = 2: row block b has its own A tile and metadata, the B tile is shared;
             // NB > 1: V-block b has its own gathered B', the A tile is shared
-            const uint32_t e_addr = e_tmem + (Cfg::MB > 1 ? 4 * b : 0) + kb;
+            // M64: block b's accumulator and metadata sit 16·b lanes into every lane quarter
+            const uint32_t lane_off = Cfg::M64 ? (static_cast<uint32_t>(16 * b) << 16) : 0u;
+            const uint32_t e_addr = e_tmem + (Cfg::MB > 1 ? 4 * b : 0) + kb + lane_off;
             const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
             // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
-            const uint64_t adesc = smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + kb * 32, 16, 1024, 2);
+            // (M64: block b's 64 rows start 8 KB into the tile)
+            const uint64_t adesc =
+                smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + (Cfg::M64 ? b * 8192 : 0) + kb * 32,
+                          16, 1024, 2);
             // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
             // K advance 32 rows = 4096 B per MMA
             // kBK: two K-major SW128 regions of BNH rows × 64 K-elements; K = 32 per MMA = 64 B
@@ -240,8 +256,8 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
               tc_mma_sp_f16_2sm(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
                                 (ks | kb) != 0 ? 1u : 0u);
             else
-              tc_mma_sp_f16(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
-                            (ks | kb) != 0 ? 1u : 0u);
+              tc_mma_sp_f16(Cfg::M64 ? d_tile + lane_off : d_tile + b * BN, adesc, bdesc, idesc | id2,
+                            e_addr & ~1u, (ks | kb) != 0 ? 1u : 0u);
           }
         }
       }
@@ -283,7 +299,13 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
   const int q = warp & 3;               // TMEM lane quarter this warp may access
   const int h = (warp - Cfg::W_EPI) >> 2;  // column half
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
-  const int r_local = 128 * static_cast<int>(rank) + 32 * q + lane;  // row within the (pair) tile
+  // row of this lane within the (pair) tile; M64: the lane half (lane >> 4) is the V-block
+  const int r_local = Cfg::M64 ? 64 * (lane >> 4) + 16 * q + (lane & 15)
+                               : 128 * static_cast<int>(rank) + 32 * q + lane;
+  // row of slot row r (0..31) of this warp's 32-row staging chunk, relative to the tile's row 0
+  auto slot_row = [&](int r) -> int {
+    return Cfg::M64 ? 64 * (r >> 4) + 16 * q + (r & 15) : 128 * static_cast<int>(rank) + 32 * q + r;
+  };
   for (int tl = 0; tl < my_tiles; ++tl) {
     int m_tile, n_tile;
     tile_coords<CG>(p, tl, m_tile, n_tile);
@@ -292,7 +314,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     tc_fence_after();
     if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row = static_cast<int64_t>(m_tile) * (128 * CG) + r_local;
-    const int b = (NB == 1) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
+    const int b = (NB == 1 || Cfg::M64) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
     const float bv = (p.bias != nullptr && row < p.R)
                          ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
                                   : __half2float(__ushort_as_half(p.bias[row])))
@@ -324,7 +346,79 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       else mbar_arrive(acce0 + 8 * ab);
     }
     const int64_t col_base = static_cast<int64_t>(n_tile) * BN + h * HC;
-    if constexpr (kCT) {
+    if (kCT && tm_c != nullptr && !(p.dbg & 4)) {
+      // token-major C through the TMA-store epilogue: lane pairs swap halves with one shuffle (the
+      // even lane then holds rows (r, r+1) of column t, the odd lane rows (r-1, r) of column t+1),
+      // each 32-bit word goes to its place in a shared-memory slot laid out as the C^T box
+      // [32 columns t][32 rows r] (64-byte rows, 64-byte swizzle; M64: two [32 t][16 r] halves of
+      // 32-byte rows, 32-byte swizzle), and one lane stores the box(es) with cp.async.bulk.tensor.
+      // (The direct path below issued a bounds-checked store per word and per peer: the epilogue
+      // then paced the V = 64 kernel, 0.19 vs 0.11 ms for row-major C at the encoder's QKV layer.)
+      const bool odd = lane & 1;
+      const int rb0 = m_tile * (128 * CG);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if (32 * c >= HC) break;
+        const uint32_t slot = stage_smem + (c % Cfg::EPI_BUFS) * Cfg::EPI_SLOT;
+        if (lane == 0) {
+          if (Cfg::EPI_BUFS == 2) bulk_wait_group_read<1>();
+          else bulk_wait_group_read<0>();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t w = pk[c][j];
+          const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, w, 1);
+          const uint32_t v = odd ? ((o >> 16) | (w & 0xFFFF0000u)) : ((w & 0xFFFFu) | (o << 16));
+          const int t = 2 * j + (odd ? 1 : 0);  // column within the chunk = slot row
+          uint32_t a;
+          if constexpr (Cfg::M64) {
+            const int wd = (lane & 15) >> 1;  // word of the 16-row half: rows 2·wd, 2·wd + 1
+            a = slot + (lane >> 4) * 1024 + t * 32 + ((((wd >> 2) ^ (t >> 2)) & 1) << 4) + (wd & 3) * 4;
+          } else {
+            const int wd = lane >> 1;
+            a = slot + t * 64 + ((((wd >> 2) ^ (t >> 1)) & 3) << 4) + (wd & 3) * 4;
+          }
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        const int tcol = static_cast<int>(col_base) + 32 * c;
+        if (lane == 0) {
+          tma_store_2d(tm_c, slot, rb0 + slot_row(0), tcol);
+          if constexpr (Cfg::M64) tma_store_2d(tm_c, slot + 1024, rb0 + slot_row(16), tcol);
+          bulk_commit_group();
+        }
+        if (p.n_peers > 0) {
+          // fused all-gather: the chunk from the slot to every peer buffer, 16-byte row segments
+          constexpr int HALVES = Cfg::M64 ? 2 : 1, RB = Cfg::M64 ? 32 : 64;  // row bytes per half
+#pragma unroll
+          for (int hh = 0; hh < HALVES; ++hh)
+#pragma unroll
+            for (int jj = 0; jj < 4 / HALVES; ++jj) {
+              const int spr = RB / 16;  // 16-byte segments per slot row
+              const int t = (32 / spr) * jj + lane / spr, sgm = lane % spr;
+              const int swz = Cfg::M64 ? ((t >> 2) & 1) : ((t >> 1) & 3);
+              uint4 o;
+              const uint32_t a = slot + hh * 1024 + t * RB + ((sgm ^ swz) << 4);
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
+              const int64_t r = rb0 + slot_row(16 * hh) + 8 * sgm;
+              const int64_t tt = tcol + t;
+              if (tt < p.T && r < p.R)
+                for (int pp = 0; pp < p.n_peers; ++pp) {
+                  uint16_t* dst = p.c_peers[pp] + tt * p.ldc + r;
+                  if (r + 8 <= p.R) {
+                    *reinterpret_cast<uint4*>(dst) = o;
+                  } else {
+                    const uint16_t* e = reinterpret_cast<const uint16_t*>(&o);
+                    for (int u = 0; u < p.R - r; ++u) dst[u] = e[u];
+                  }
+                }
+            }
+        }
+      }
+      if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(10, tl);
+    } else if constexpr (kCT) {
       // token-major C (C^T[t][r]): the warp's 32 lanes hold 32 consecutive rows of columns t, t+1
       // (one packed word). Lane pairs swap halves with one shuffle so the even lane stores rows
       // (r, r+1) of column t and the odd lane rows (r-1, r) of column t+1 as 32-bit words: every
@@ -358,7 +452,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       // conflict-free), then one lane stores the box with cp.async.bulk.tensor; the TMA unit
       // clips the ragged R / T edges. Slots are double-buffered when shared memory allows: a slot
       // is rewritten only once the store issued from it has read it.
-      const int row_base = m_tile * (128 * CG) + 128 * static_cast<int>(rank) + 32 * q;
+      const int row_base = m_tile * (128 * CG);
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         if (32 * c >= HC) break;
@@ -377,7 +471,13 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
         fence_proxy_async_smem();  // the generic-proxy writes, visible to the bulk-copy engine
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(tm_c, slot, static_cast<int32_t>(col_base + 32 * c), row_base);
+          if constexpr (Cfg::M64) {
+            // the two V-blocks' 16-row halves (the C map's box is 16 rows for M64)
+            tma_store_2d(tm_c, slot, static_cast<int32_t>(col_base + 32 * c), row_base + slot_row(0));
+            tma_store_2d(tm_c, slot + 1024, static_cast<int32_t>(col_base + 32 * c), row_base + slot_row(16));
+          } else {
+            tma_store_2d(tm_c, slot, static_cast<int32_t>(col_base + 32 * c), row_base + slot_row(0));
+          }
           bulk_commit_group();
         }
         if (p.n_peers > 0) {
@@ -390,7 +490,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
             uint4 o;
             const uint32_t a = slot + r * 64 + ((sgm ^ ((r >> 1) & 3)) * 16);
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
-            const int64_t orow = row_base + r;
+            const int64_t orow = row_base + slot_row(r);
             const int64_t ocol = col_base + 32 * c + 8 * sgm;
             if (orow < p.R && ocol < p.T)
               for (int pp = 0; pp < p.n_peers; ++pp)
@@ -403,7 +503,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       // transpose each 32-row × 32-column chunk through a 2 KB shared-memory slot so that every
       // store instruction writes 8 rows × 64 contiguous bytes (full sectors) instead of 32 rows ×
       // 16 bytes; 16-byte segments XOR-swizzled by row to keep both passes bank-conflict free
-      const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG) + 128 * static_cast<int>(rank) + 32 * q;
+      const int64_t row_base = static_cast<int64_t>(m_tile) * (128 * CG);
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         if (32 * c >= HC) break;
@@ -420,7 +520,7 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
           uint4 o;
           const uint32_t a = stage_smem + r * 64 + ((sgm ^ ((r >> 1) & 3)) * 16);
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "r"(a) : "memory");
-          const int64_t orow = row_base + r;
+          const int64_t orow = row_base + slot_row(r);
           const int64_t ocol = col_base + 32 * c + 8 * sgm;
           // ablation 8192: the shared-memory transposes without the global stores
           if (orow < p.R && ocol < p.T && !(p.dbg & 8192)) *reinterpret_cast<uint4*>(p.C + orow * p.ldc + ocol) = o;
@@ -650,7 +750,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     prefetch_tmap(&tm_values);
     prefetch_tmap(&tm_b);
     if constexpr (Cfg::PRE) prefetch_tmap(&tm_e);
-    if (!kCT && p.tma_c) prefetch_tmap(&tm_c);
+    if (p.tma_c) prefetch_tmap(&tm_c);
   }
   if (warp == Cfg::W_MMA) {
     if constexpr (CG == 2) tmem_alloc_2sm<512>(smem_u32(tmem_base_slot));
@@ -738,6 +838,8 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     // ablation flags (p.dbg, tools only): 1 no B loads, 16 no A load, 2048 no metadata load
     const uint32_t tx = CG * ((p.dbg & 16 ? 0 : Cfg::A_BYTES) + (p.dbg & 1 ? 0 : NB * Cfg::B_BYTES) +
                               (p.dbg & 2048 ? 0 : Cfg::E_BYTES));
+    // the last k-stage gathers only the groups its MMAs read (8·last_kb of 32)
+    const uint32_t tx_last = tx - CG * (p.dbg & 1 ? 0u : static_cast<uint32_t>(NB * Cfg::NCH * 512 * (32 - 8 * p.last_kb)));
     for (int it0 = 0; it0 < total; it0 += kPrefetch) {
 #pragma unroll
       for (int jj = 0; jj < kPrefetch; ++jj) {
@@ -748,7 +850,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
           const uint32_t fbar = (CG == 2) ? mapa_shared(full0 + 8 * stage, 0) : full0 + 8 * stage;
           if (warp == 0 && lane == 0) {
             VENOM_TRACE_EVENT(0, it);
-            if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, tx);
+            if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * stage, ks == p.num_ks - 1 ? tx_last : tx);
             if (!(p.dbg & 16)) {
 #pragma unroll
               for (int mb = 0; mb < Cfg::MB; ++mb) {
@@ -764,15 +866,28 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
               for (int mb = 0; mb < Cfg::MB; ++mb) {
                 const uint32_t edst = sbase + Cfg::A_BYTES + NB * Cfg::B_BYTES + mb * Cfg::E_BLOCK;
                 const int eblk = ((m_tile * Cfg::MB + mb) * CG + static_cast<int>(rank)) * p.num_ks + ks;
-                if constexpr (CG == 2) tma_load_2d_2sm(edst, &tm_e, fbar, 0, eblk, pol_a);
-                else tma_load_2d(edst, &tm_e, fbar, 0, eblk, pol_a);
+                if constexpr (CG == 2) {
+                  tma_load_2d_2sm(edst, &tm_e, fbar, 0, eblk, pol_a);
+                } else if constexpr (Cfg::M64) {
+                  // the M = 64 lane order: 16-lane group x + 4y of the block lands at 2x + y (a
+                  // 4-D map [block][x: 4, 256 B apart][y: 2, 1 KB apart][256 B], box order y, x)
+                  if (p.e4d) {
+                    tma_load_4d(edst, &tm_e, fbar, 0, 0, 0, eblk, pol_a);
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      tma_load_2d(edst + 256 * (2 * (j & 3) + (j >> 2)), &tm_e, fbar, 0, 8 * eblk + j, pol_a);
+                  }
+                } else {
+                  tma_load_2d(edst, &tm_e, fbar, 0, eblk, pol_a);
+                }
               }
             }
           }
           if (!(p.dbg & 1)) {
 #pragma unroll
             for (int j = 0; j < Cfg::LANE_OPS; ++j) {
-              if (!olive[j]) continue;
+              if (!olive[j] || (ks == p.num_ks - 1 && oq[j] >= 8 * p.last_kb)) continue;
               const int gg = ks * Cfg::KG + oq[j];
               const uint32_t w = cw[jj][j];
               int r[4];
@@ -807,14 +922,17 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
     else epilogue_role<Cfg, kBF16, CG, kCT, kGELU>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot,
-                                                   (!kCT && p.tma_c) ? &tm_c : nullptr);
+                                                   p.tma_c ? &tm_c : nullptr);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========
     // TMEM lane L of one K=32 MMA holds rows m = (L&7) + 16(L>>4) (low half-word) and m+8 (high
     // half-word), each for K-half k1 = (L>>3)&1: the 16 bits of groups 4·k1 .. 4·k1+3. The warp
     // writes its lane quarter (warp % 4) with tcgen05.st: no shared memory, no proxy fence.
     const int qd = warp & 3;
-    const int L = 32 * qd + lane;
+    // TMEM lane 32·qd + lane holds the M = 128 order's lane L; M64 interleaves the two 64-row
+    // blocks' halves (physical lane bits [6:5] = L bits [5:4], bit 4 = L bit 6)
+    const int Pl = 32 * qd + lane;
+    const int L = Cfg::M64 ? (Pl & 15) + 16 * ((Pl >> 5) & 3) + 64 * ((Pl >> 4) & 1) : Pl;
     const int total_meta = (p.dbg & 256) ? 0 : total;
     const int m_a = (L & 7) + 16 * (L >> 4);
     const int k1 = (L >> 3) & 1;

@@ -128,7 +128,9 @@ venom_status_t run_gather(int NBg, int pair, int tile_t, const CUtensorMap& tv, 
     if (tile_t == 128) return run_spmm<SpmmCfg<1, 128, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
     if (tile_t == 64) return run_spmm<SpmmCfg<1, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else if (NBg == 2) {
-    if (tile_t == 128) return run_spmm<SpmmCfg<2, 128, 2, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    // 11 gather-issuing warps as for V = 128 (8 with the 4 metadata warps: 768 threads would cap
+    // registers at 80)
+    if (tile_t == 128) return run_spmm<SpmmCfg<2, 128, 2, PRE ? 11 : 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
     if (tile_t == 64) return run_spmm<SpmmCfg<2, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else {
     if (tile_t == 64) return run_spmm<SpmmCfg<4, 64, 2, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);

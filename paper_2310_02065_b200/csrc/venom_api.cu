@@ -535,6 +535,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   p.bk = bk ? 1 : 0;
   p.act = act;
   p.tma_c = 0;
+  p.e4d = 0;
+  p.last_kb = 4;
   p.n_peers = 0;
   for (int i = 0; i < venom::kMaxPeers; ++i) p.c_peers[i] = nullptr;
   if (opts && opts->n_peers != 0) {
@@ -598,6 +600,9 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   // box [NCH][128][64] lands the CTA's whole B' stage in the chunked SW128 layout.
   const bool contiguous = (f.m == 4);
   p.num_ks = static_cast<int>((G + 31) / 32);
+  // K = 32 MMAs (8 groups each) that carry real groups in the last k-stage: the rest are neither
+  // gathered nor multiplied (e.g. G = 104: 8 of the last stage's 32 groups)
+  p.last_kb = static_cast<int>((G - 32 * (static_cast<int64_t>(p.num_ks) - 1) + 7) / 8);
   const int NBg = contiguous ? 1 : NB;  // M = 4 ignores V (column_idx is the identity)
   const bool pair_ok = NBg == 1 && (contiguous || V % 256 == 0);
   const int pair = (opts && opts->cta_pair) ? opts->cta_pair : (pair_ok ? 2 : 1);
@@ -647,10 +652,24 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   // staging layout); token-major C keeps its direct stores
   CUtensorMap tc = tv;
   p.tma_c = 0;
-  if (!ct) {
+  if (ct) {
+    // token-major C^T [T rows][R]: boxes of 32 columns t × 32 rows r (64-byte swizzle), or × 16
+    // rows r for V = 64 (each warp holds two 16-row halves; 32-byte swizzle)
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(T)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldc)};
+    cuuint32_t box[2] = {NBg == 2 ? 16u : 32u, 32};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            NBg == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.tma_c = 1;
+    else
+      tc = tv;
+  } else {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(R)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldc)};
-    cuuint32_t box[2] = {32, 32};
+    // V = 64 (two M = 64 blocks per tile): a warp's 32 lanes hold two 16-row halves -> 16-row boxes
+    cuuint32_t box[2] = {32, NBg == 2 ? 16u : 32u};
     cuuint32_t es[2] = {1, 1};
     if (enc(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
@@ -669,7 +688,31 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   // 128 rows would cost the TMA unit 128 row requests per stage)
   if (!aligned(meta_tc, 16)) return VENOM_ERR_INVALID_ARGUMENT;
   CUtensorMap te;
-  {
+  p.e4d = 0;
+  if (NBg == 2) {
+    // V = 64: the kernel's TMEM lane order for two M = 64 blocks is a permutation of the stored
+    // 16-lane groups (group x + 4y of a block -> 2x + y, spmm_kernel.cuh M64); a 4-D map with
+    // swapped strides does it in one TMA op: dims [256 B][y: 2, 1 KB][x: 4, 256 B][blocks, 2 KB]
+    const int64_t blocks = ((R + 127) / 128) * p.num_ks;
+    cuuint64_t dims[4] = {32, 2, 4, static_cast<cuuint64_t>(blocks)};
+    cuuint64_t strides[3] = {1024, 256, 2048};
+    cuuint32_t box[4] = {32, 2, 4, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<uint8_t*>(meta_tc), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      p.e4d = 1;
+    } else {
+      // fallback: 256-byte rows [blocks·8][32] u64, eight row loads per stage
+      cuuint64_t d2[2] = {32, static_cast<cuuint64_t>(blocks * 8)};
+      cuuint64_t s2[1] = {256};
+      cuuint32_t b2[2] = {32, 1};
+      if (enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(meta_tc), d2, s2, b2, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return VENOM_ERR_CUDA;
+    }
+  } else {
     const int64_t blocks = ((R + 127) / 128) * p.num_ks;
     cuuint64_t dims[2] = {256, static_cast<cuuint64_t>(blocks)};
     cuuint64_t strides[1] = {2048};

@@ -44,6 +44,12 @@ WORKLOADS = {
     "fig6_1024x4160x4096_128:2:40": dict(R=1024, K=4160, T=4096, V=128, M=40, cfg=1),
     "fig6_1024x4800x4096_128:2:100": dict(R=1024, K=4800, T=4096, V=128, M=100, cfg=1),
     "gpt3_ffn_12288x49152x8192_128:2:16": dict(R=12288, K=49152, T=8192, V=128, M=16, cfg=3),
+    # the sparse BERT-large encoder's linear layers (configs[4]: 64:2:10, batch 32 x seq 512;
+    # K padded to a multiple of 8M, reading #11)
+    "enc_qkv_3072x1040x16384_64:2:10": dict(R=3072, K=1040, T=16384, V=64, M=10, cfg=4),
+    "enc_o_1024x1040x16384_64:2:10": dict(R=1024, K=1040, T=16384, V=64, M=10, cfg=4),
+    "enc_ffn1_4096x1040x16384_64:2:10": dict(R=4096, K=1040, T=16384, V=64, M=10, cfg=4),
+    "enc_ffn2_1024x4160x16384_64:2:10": dict(R=1024, K=4160, T=16384, V=64, M=10, cfg=4),
 }
 
 

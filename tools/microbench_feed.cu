@@ -35,6 +35,8 @@ struct Cfg {
   int with_a;   // 16 KB A box per stage (8 KB when rows == 64)
   int tile;     // B' by contiguous tile boxes of `tile` rows × 64 columns instead of gathers
   int mma;      // consumer issues the stage's sparse MMAs
+  int cpa;      // the non-TMA warps use cp.async (16 B per lane, completion via
+                // cp.async.mbarrier.arrive.noinc; no register staging, several stages in flight)
   int iters;
 };
 
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(512, 1) feed_kernel(const __grid_constant__ CU
   const uint32_t salt = blockIdx.x * 7919u;
   if (threadIdx.x == 0) {
     for (int s = 0; s < c.S; ++s) {
-      mbar_init(smem_u32(&full[s]), 1 + c.nlw);
+      mbar_init(smem_u32(&full[s]), 1 + (c.cpa ? 32 * c.nlw : c.nlw));
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(&drain), 1);
@@ -122,6 +124,25 @@ __global__ void __launch_bounds__(512, 1) feed_kernel(const __grid_constant__ CU
         }
       }
     }
+  } else if (warp < c.ntw + c.nlw && c.cpa) {
+    // ------------------------------------------------ cp.async warps: rows [rt, rows), one 512-byte
+    // row per warp instruction; the stage's completion is signalled asynchronously, so a warp moves
+    // on to the next stage without waiting for its copies (in flight: up to S stages)
+    const int lw = warp - c.ntw;
+    const int chn = lane >> 3, unit = lane & 7;
+    for (int it = 0; it < c.iters; ++it) {
+      const int s = it % c.S;
+      mbar_wait(smem_u32(&empty[s]), ((it / c.S) & 1) ^ 1);
+      const uint32_t sb = s0 + s * stage_bytes + a_bytes;
+      for (int j = c.rt + lw; j < c.rows; j += c.nlw) {
+        const int row = brow(it, j, c.rows, salt);
+        const uint16_t* src = Bp + static_cast<size_t>(row) * TCOLS + band + chn * 64 + unit * 8;
+        const uint32_t dst = sb + chn * chunk + j * 128 + ((unit ^ (j & 7)) << 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp < c.ntw + c.nlw) {
     // ------------------------------------------------ LDG warps: rows [rt, rows) of every stage
     const int lw = warp - c.ntw;
@@ -161,6 +182,7 @@ __global__ void __launch_bounds__(512, 1) feed_kernel(const __grid_constant__ CU
     for (int it = 0; it < c.iters; ++it) {
       const int s = it % c.S;
       mbar_wait(smem_u32(&full[s]), (it / c.S) & 1);
+      if (c.cpa) fence_proxy_async_smem();  // cp.async wrote through the generic proxy
       tc_fence_after();
       if (c.mma) {
         const uint32_t sb = s0 + s * stage_bytes;
@@ -232,8 +254,15 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 1024);
   cudaFuncSetAttribute(feed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-  // {S, rows, rt, ntw, nlw, with_a, tile, mma}
+  // {S, rows, rt, ntw, nlw, with_a, tile, mma, cpa}
   std::vector<Cfg> cases = {
+      // cp.async only, and cp.async beside gather4 (round 2b)
+      {2, 128, 0, 1, 8, 1, 0, 0, 1}, {2, 128, 0, 1, 14, 1, 0, 0, 1}, {5, 64, 0, 1, 14, 1, 0, 0, 1},
+      {3, 96, 0, 1, 14, 1, 0, 0, 1},
+      {2, 128, 96, 8, 6, 1, 0, 0, 1}, {2, 128, 80, 8, 6, 1, 0, 0, 1}, {2, 128, 64, 8, 6, 1, 0, 0, 1},
+      {2, 128, 96, 11, 4, 1, 0, 0, 1}, {2, 128, 64, 11, 4, 1, 0, 0, 1},
+      {2, 128, 96, 8, 6, 1, 0, 1, 1}, {2, 128, 80, 8, 6, 1, 0, 1, 1}, {2, 128, 64, 8, 6, 1, 0, 1, 1},
+      {2, 128, 128, 11, 0, 1, 0, 1, 0},
       // gather4 only (80 KB stages as the GPT-3 kernel: A + 64 KB B'; 40 KB at K' = 64)
       {2, 128, 128, 4, 0, 1, 0, 0}, {2, 128, 128, 8, 0, 1, 0, 0}, {2, 128, 128, 15, 0, 1, 0, 0},
       {5, 64, 64, 4, 0, 1, 0, 0}, {5, 64, 64, 8, 0, 1, 0, 0}, {5, 64, 64, 15, 0, 1, 0, 0},
@@ -276,9 +305,9 @@ int main() {
       double avgc = 0;
       for (int i = 0; i < grid; ++i) avgc += double(cyc[i]) / grid;
       const double bytes = double(c.iters) * stage;  // per CTA
-      printf("grid=%3d S=%d rows=%3d gather_rows=%3d tma_warps=%2d ldg_warps=%2d A=%d tile=%d mma=%d: "
+      printf("grid=%3d S=%d rows=%3d gather_rows=%3d tma_warps=%2d %s_warps=%2d A=%d tile=%d mma=%d: "
              "%6.1f B/cycle/SM  %6.1f B/ns/SM  %6.2f TB/s chip  stage %6.0f cycles %s\n",
-             grid, c.S, c.rows, c.tile ? 0 : c.rt, c.ntw, c.nlw, c.with_a, c.tile, c.mma, bytes / avgc,
+             grid, c.S, c.rows, c.tile ? 0 : c.rt, c.ntw, c.cpa ? "cpa" : "ldg", c.nlw, c.with_a, c.tile, c.mma, bytes / avgc,
              bytes * grid / (ms * 1e6) / grid, bytes * grid / (ms * 1e9), avgc / c.iters,
              err == cudaSuccess ? "" : cudaGetErrorString(err));
       if (err != cudaSuccess) return 1;

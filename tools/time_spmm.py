@@ -18,6 +18,8 @@ def main():
     st = torch.cuda.current_stream(dev)
     for spec in sys.argv[2:] or [""]:
         kw = {k: int(v) for k, v in (x.split("=") for x in spec.split(",") if x)}
+        if kw.get("transposed_out"):  # token-major C^T [T, R]
+            kw["out"] = torch.empty((L.T, L.w["R"]), dtype=L.C.dtype, device=dev)
         for _ in range(3):
             L.spmm(**kw)
         ts = []
