@@ -286,6 +286,8 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 // tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
 // kGELU: GELU (erf form, torch.nn.functional.gelu) after the bias, in fp32 before the rounding —
 // a separate instantiation (a runtime activation branch slowed every SpMM)
+// (A Chebyshev erfc with a MUFU reciprocal and exp measured no faster than erff: the GELU
+// epilogue's cost is its issue share beside the producers, not erff's length.)
 __device__ __forceinline__ float gelu_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
 template <class Cfg, bool kBF16, int CG = 1, bool kCT = false, bool kGELU = false>

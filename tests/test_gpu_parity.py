@@ -333,8 +333,15 @@ SPMM_CASES = [
     (384, 512, 264, 64, 4, BF16, False, 256),  # 2:4, half-filled cluster tile, T tail
     (512, 1024, 384, 128, 16, F16, True, 192),
     (512, 2048, 256, 128, 32, BF16, False, 64),
-    (256, 1024, 256, 64, 8, F16, True, 128),   # V=64 tile 128 (single accumulator)
+    (256, 1024, 256, 64, 8, F16, True, 128),   # V=64 tile 128
     (128, 4096, 64, 128, 16, F16, False, 0),   # long K
+    # V = 64 as two M = 64 MMAs on the TMEM lane halves (spmm_kernel.cuh M64): a single 64-row
+    # block (the tile's second half is padding), 2.5 row tiles, and last k-stages of 4 / 16 / 12
+    # real groups (G = 36, 112, 44: the MMAs and gathers past them are skipped)
+    (64, 288, 72, 64, 8, BF16, True, 0),
+    (320, 960, 200, 64, 10, F16, True, 0),
+    (448, 1120, 128, 64, 10, BF16, False, 64),
+    (192, 880, 136, 64, 20, F16, True, 128),
 ]
 
 
@@ -636,7 +643,44 @@ def test_sparse_encoder_matches_dense_on_pruned_weights():
            for L in dense]
     yd = enc.dense_forward(cfg, d32, x.float())
     rel = float((ys - yd).norm() / yd.norm())
-    assert rel <= 1e-2, rel
+    # composite tolerance: the sparse encoder rounds to fp16 at ~8 points per layer (4 SpMM outputs,
+    # SDPA, two LayerNorms, the attention transpose), the reference runs in fp32; each rounding adds
+    # an RMS relative error of about 2^-11/sqrt(3) = 2.8e-4, and LayerNorm renormalises instead of
+    # compounding, so 2 layers give about sqrt(16)·2.8e-4 = 1.1e-3 plus SDPA's own fp16 softmax;
+    # 5e-3 leaves 2-4x headroom over that (measured: see the assertion message)
+    assert rel <= 5e-3, rel
+
+
+@pytest.mark.parametrize("dt", [F16])
+def test_encoder_linear_layers_vs_oracle(dt):
+    """§8(f) rank 1: each of an encoder layer's four V:N:M linear layers, called exactly as the
+    encoder calls it (QKV / O / FFN2 token-major C, FFN1 with the GELU epilogue; 64:2:10 with K
+    padded to 1040 / 4160), against the oracle's fp64 product on the oracle's own compression of
+    the same padded weight, at the north-star tolerance."""
+    import math
+    from paper_2310_02065_b200 import encoder as enc
+    cfg = enc.EncoderConfig(layers=1, batch=1, seq=264)  # T = 264: two 128-column tiles + a tail
+    W = enc.init_weights(cfg, torch.device("cuda"), seed=11)
+    model = enc.SparseEncoder(cfg, W)
+    L, lw = model.layers[0], W[0]
+    T = cfg.tokens
+    erf = np.vectorize(math.erf)
+    for key, wkey, bkey, tm, gelu in (("qkv", "wqkv", "bqkv", True, False), ("o", "wo", "bo", True, False),
+                                      ("f1", "w1", "b1", False, True), ("f2", "w2", "b2", True, False)):
+        lin = L[key]
+        w = lw[wkey].cpu()
+        Wp = torch.zeros((lin.out_f, lin.K), dtype=torch.float16)
+        Wp[:, :lin.in_f] = w
+        parts = oracle.compress(Wp.view(torch.int16).numpy().view(np.uint16), F16, V=cfg.V, M=cfg.M)
+        xb = synth.gaussian((lin.K, T), 1.0, F16, 60 + len(key))
+        xb[lin.in_f:] = 0  # the encoder's zero K-padding rows
+        bits_b = lw[bkey].cpu().view(torch.int16).numpy().view(np.uint16)
+        ref = oracle.spmm(*parts, lin.out_f, lin.K, F16, cfg.V, cfg.M, xb, bias=bits_b)
+        if gelu:
+            ref = 0.5 * ref * (1.0 + erf(ref / math.sqrt(2.0)))
+        out = torch.empty((T, lin.out_f) if tm else (lin.out_f, T), dtype=torch.float16, device="cuda")
+        got = lin(to_dev(xb, F16), out=out, token_major=tm, gelu=gelu)
+        check_spmm(got.t().contiguous() if tm else got, ref, F16)
 
 
 # ------------------------------------------------------------------ masked compression + energy
@@ -765,6 +809,7 @@ def test_spmm_degenerate_shapes():
 
 @pytest.mark.parametrize("R,K,T,V,M,dt,bias", [
     (192, 640, 136, 64, 10, F16, True),    # encoder's 64:2:10 (gathered, two V-blocks per tile)
+    (320, 960, 200, 64, 10, BF16, False),  # V = 64, 2.5 row tiles, T tail (16-row C^T boxes)
     (384, 1024, 200, 128, 16, BF16, False),
     (512, 1024, 264, 128, 4, F16, True),   # 2:4 (contiguous, CTA pair)
     (130, 256, 64, 13, 8, F16, True),      # dense-K-only V -> rejected for token-major C
