@@ -46,7 +46,7 @@ typedef enum {
   VENOM_ERR_NON_DIVISIBLE_ROWS = 2,  /* V does not divide R              */
   VENOM_ERR_NON_DIVISIBLE_COLS = 3,  /* M does not divide K              */
   VENOM_ERR_UNSUPPORTED_PATTERN = 4, /* N != 2, M < 4, M > 256; spmm: V not in {32,64} ∪ 128ℕ,
-                                        G % 4 != 0                                               */
+                                        G % 4 != 0 without the padded execution form            */
   VENOM_ERR_UNSUPPORTED_DTYPE = 5,
   VENOM_ERR_NON_FINITE = 6,          /* device-reported (finite inputs only)         */
   VENOM_ERR_CORRUPT_METADATA = 7,    /* device-reported: m-indices not ascending, column_idx not
@@ -138,7 +138,8 @@ venom_status_t venom_decompress(const void* values, const uint8_t* metadata,
  *   is read (no opts->metadata_tc); dense-K additionally needs column_idx 16-byte aligned (a
  *   misaligned view returns VENOM_ERR_INVALID_ARGUMENT instead of faulting on the device);
  *   and at least one strategy applies:
- *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0
+ *     gather : (V in {32, 64} or V % 128 == 0 or M == 4) and G = K/M with G % 4 == 0, or any G
+ *              with opts->metadata_tc and opts->values_padded (venom_pad_values)
  *     dense-K: M in {4, 8, 16, 32} and G % 4 == 0 (any V)
  *   The library picks the faster applicable strategy (see venom_spmm_opts_t).
  * R == 0 or T == 0: nothing to compute, VENOM_OK with no launch (leading dimensions are not checked).
@@ -249,6 +250,10 @@ typedef struct {
                         / contiguous kernel, one accumulator per CTA (dense-K and tile_t 240 return
                         VENOM_ERR_INVALID_ARGUMENT). NULL / 0: none. */
   int32_t n_peers;     /* 0..8 */
+  const void* values_padded;  /* nullable DEVICE pointer: the operand's values with each row padded
+                        to a multiple of 4 groups (venom_pad_values). Needed, with metadata_tc, when
+                        G = K/M is not a multiple of 4: the values' TMA map needs a 16-byte row
+                        pitch (4·G bytes otherwise). Ignored when G % 4 == 0. 16-byte aligned. */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,
@@ -266,13 +271,24 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
  * uint32[ceil(R/128)][ceil(G/32)][128 lanes][4 MMAs], G = K/M; lane L, MMA kb holds the 16 bits of
  * groups 32·ks + 8·kb + 4·((L>>3)&1) .. +3 of row (L&7) + 16·(L>>4) (low half) and of that row + 8
  * (high half); rows >= R and groups >= G are filled with the zero-value code 0x4 (m-indices 0,1).
- * venom_metadata_tc_bytes returns the size in bytes (-1 for an invalid format). Requires G % 4 == 0
- * (VENOM_ERR_UNSUPPORTED_PATTERN otherwise). metadata_tc: caller-owned device buffer, 16-byte
- * aligned. Metadata validity is not checked (use venom_decompress with dev_status).
+ * venom_metadata_tc_bytes returns the size in bytes (-1 for an invalid format). Any G (a partial
+ * last 4-group word is completed with 0x4 nibbles). metadata_tc: caller-owned device buffer,
+ * 16-byte aligned. Metadata validity is not checked (use venom_decompress with dev_status).
  */
 int64_t venom_metadata_tc_bytes(int64_t R, int64_t K, venom_format_t f);
 venom_status_t venom_order_metadata(const uint8_t* metadata, int64_t R, int64_t K, venom_format_t f,
                                     uint8_t* metadata_tc, venom_stream_t stream);
+
+/*
+ * Values with a padded row pitch — the execution form for G = K/M not a multiple of 4 (the K'
+ * tail the paper's K sweeps reach): values_padded = dtype[R][G4][2] with
+ * G4 = ceil(G/4)·4; groups >= G are +0.0 (they meet the 0x4 metadata of venom_order_metadata and
+ * zero-filled rows of B, so they add nothing). venom_values_padded_bytes returns R·G4·4 (-1 for
+ * an invalid format). values: 4-byte aligned; values_padded: caller-owned, 16-byte aligned.
+ */
+int64_t venom_values_padded_bytes(int64_t R, int64_t K, venom_format_t f);
+venom_status_t venom_pad_values(const void* values, int64_t R, int64_t K, venom_format_t f,
+                                void* values_padded, venom_stream_t stream);
 
 /* Number of kernels venom_spmm / venom_compress / venom_decompress launch per call (1 each). */
 int32_t venom_kernels_per_call(void);

@@ -31,7 +31,7 @@ STATUS_NAMES = {
 }
 EXPORTED = ["venom_compressed_sizes", "venom_compress", "venom_decompress", "venom_spmm",
             "venom_spmm_ex", "venom_expand_2to4", "venom_compress_2to4", "venom_prefer_2to4",
-            "venom_metadata_tc_bytes",
+            "venom_metadata_tc_bytes", "venom_values_padded_bytes", "venom_pad_values",
             "venom_order_metadata", "venom_kernels_per_call", "venom_status_string",
             "venom_version", "venom_compress_masked", "venom_energy",
             # include/venom_encoder.h (encoder layout helpers, not the V:N:M method)
@@ -53,7 +53,8 @@ class _Opts(ctypes.Structure):
                 ("strategy", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
                 ("metadata_tc", ctypes.c_void_p), ("c_transposed", ctypes.c_int32),
                 ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32), ("group_n", ctypes.c_int32),
-                ("c_peers", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_int32)]
+                ("c_peers", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_int32),
+                ("values_padded", ctypes.c_void_p)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -82,6 +83,10 @@ def lib() -> ctypes.CDLL:
         L.venom_metadata_tc_bytes.argtypes = [I64, I64, _Format]
         L.venom_metadata_tc_bytes.restype = I64
         L.venom_order_metadata.argtypes = [P, I64, I64, _Format, P, P]
+        L.venom_values_padded_bytes.argtypes = [I64, I64, _Format]
+        L.venom_values_padded_bytes.restype = I64
+        L.venom_pad_values.argtypes = [P, I64, I64, _Format, P, P]
+        L.venom_pad_values.restype = ctypes.c_int
         L.venom_compress_2to4.argtypes = [P, I64, I64, I64, ctypes.c_int, _Format, P, P, P, P, P, P, P]
         L.venom_compress_masked.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, _Format, P, P, P, P, P]
         L.venom_energy.argtypes = [P, I64, I64, I64, P, I64, ctypes.c_int, P, P]
@@ -135,6 +140,7 @@ class VNMTensor:
     M: int
     N: int = 2
     metadata_tc: Optional[torch.Tensor] = None  # uint8, tensor-core order (order_metadata)
+    values_padded: Optional[torch.Tensor] = None  # rows padded to 4 groups (pad_values; G % 4 != 0)
 
     @property
     def dtype(self) -> torch.dtype:
@@ -306,6 +312,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     if bias is not None:
         assert bias.dtype == x.dtype and bias.is_contiguous() and bias.numel() == x.R
     mtc = x.metadata_tc.data_ptr() if (use_metadata_tc and x.metadata_tc is not None) else None
+    vpad = x.values_padded.data_ptr() if (mtc is not None and x.values_padded is not None) else None
     peers = None
     if c_peers:
         # fused all-gather: device addresses (ints or tensors) of the peer output slices
@@ -314,7 +321,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
                  1 if b_kmajor else 0, 1 if gelu else 0, group_n,
                  ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p)) if peers is not None else None,
-                 len(c_peers) if c_peers else 0)
+                 len(c_peers) if c_peers else 0, vpad)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
                              ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
                              ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),
@@ -376,6 +383,24 @@ def order_metadata(x: VNMTensor, out: Optional[torch.Tensor] = None) -> VNMTenso
                                     ctypes.c_void_p(out.data_ptr()), _stream(x.metadata.device))
     _check(st, "venom_order_metadata")
     x.metadata_tc = out
+    if (x.K // x.M) % 4 != 0:
+        pad_values(x)  # the K' tail's other execution-form array
+    return x
+
+
+def pad_values(x: VNMTensor) -> VNMTensor:
+    """Attach the values with rows padded to a multiple of 4 groups (include/venom.h
+    venom_pad_values) to x, in place: with metadata_tc, spmm then runs any G = K/M (a K' tail)."""
+    n = lib().venom_values_padded_bytes(x.R, x.K, x.fmt())
+    if n < 0:
+        raise VenomError(4, "venom_values_padded_bytes")
+    buf = x.values_padded
+    if buf is None or buf.numel() * buf.element_size() != max(n, 16):
+        buf = torch.empty(max(n, 16) // 2, dtype=x.dtype, device=x.values.device)
+    st = lib().venom_pad_values(ctypes.c_void_p(x.values.data_ptr()), x.R, x.K, x.fmt(),
+                                ctypes.c_void_p(buf.data_ptr()), _stream(x.values.device))
+    _check(st, "venom_pad_values")
+    x.values_padded = buf
     return x
 
 

@@ -987,8 +987,23 @@ __global__ void __launch_bounds__(256) vnm_order_metadata_kernel(const uint8_t* 
                                                                  uint32_t* __restrict__ out) {
   // thread per output word: idx = ((mt·num_ks + ks)·128 + L)·4 + kb; metadata rows are G/2 bytes
   // (G % 4 == 0), so every 4-group chunk is one aligned 16-bit word
-  const int64_t meta_row2 = G / 4;  // 16-bit words per metadata row
+  // G % 4 == 0: metadata rows are G/2 bytes, every 4-group chunk one aligned 16-bit word; any
+  // other G: the nibbles are read one byte at a time and groups >= G get the 0x4 code
+  const int64_t meta_row = (G + 1) / 2;
+  const bool words = (G % 4) == 0;
   const uint16_t* m16 = reinterpret_cast<const uint16_t*>(metadata);
+  auto quad = [&](int64_t row, int64_t g0) -> uint32_t {  // nibbles of groups g0 .. g0+3
+    if (row >= R || g0 >= G) return 0x4444u;
+    if (words) return __ldg(m16 + row * (meta_row / 2) + g0 / 4);
+    uint32_t h = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int64_t g = g0 + t;
+      const uint32_t nib = g < G ? (__ldg(metadata + row * meta_row + g / 2) >> (4 * (g & 1))) & 0xFu : 0x4u;
+      h |= nib << (4 * t);
+    }
+    return h;
+  };
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int kb = static_cast<int>(idx & 3);
@@ -996,13 +1011,20 @@ __global__ void __launch_bounds__(256) vnm_order_metadata_kernel(const uint8_t* 
     const int64_t blk = idx >> 9;  // mt * num_ks + ks
     const int64_t ks = blk % num_ks, mt = blk / num_ks;
     const int64_t ra = mt * 128 + (L & 7) + 16 * (L >> 4), rb = ra + 8;
-    const int64_t w16 = ks * 8 + kb * 2 + ((L >> 3) & 1);  // 16-bit word of groups 4·w16 .. +3
-    uint32_t lo = 0x4444u, hi = 0x4444u;
-    if (w16 < meta_row2) {
-      if (ra < R) lo = __ldg(m16 + ra * meta_row2 + w16);
-      if (rb < R) hi = __ldg(m16 + rb * meta_row2 + w16);
-    }
-    out[idx] = lo | (hi << 16);
+    const int64_t g0 = 4 * (ks * 8 + kb * 2 + ((L >> 3) & 1));  // groups g0 .. g0 + 3
+    out[idx] = quad(ra, g0) | (quad(rb, g0) << 16);
+  }
+}
+
+// Values with the row pitch padded to G4 = ceil(G/4)·4 groups (venom_pad_values, the execution form
+// for G % 4 != 0): thread per output group (two 16-bit values as one word), +0.0 past G.
+__global__ void __launch_bounds__(256) vnm_pad_values_kernel(const uint32_t* __restrict__ values, int64_t R,
+                                                             int64_t G, int64_t G4, uint32_t* __restrict__ out) {
+  const int64_t total = R * G4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / G4, g = i - row * G4;
+    out[i] = g < G ? __ldg(values + row * G + g) : 0u;
   }
 }
 

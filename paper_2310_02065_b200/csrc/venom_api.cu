@@ -448,7 +448,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (dt != VENOM_F16 && dt != VENOM_BF16) return VENOM_ERR_UNSUPPORTED_DTYPE;
   const int V = f.v;
   const int64_t G = K / f.m;
-  const bool can_gather = (f.m == 4 || V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0);
+  // G % 4 != 0 (a K' tail): the values' TMA map needs the padded execution form, and the
+  // canonical metadata (16-bit words) cannot be read by the kernel: metadata_tc is required
+  const bool padded = (G % 4 != 0) && opts && opts->values_padded && opts->metadata_tc;
+  const bool can_gather = (f.m == 4 || V == 32 || V == 64 || V % 128 == 0) && (G % 4 == 0 || padded);
   // dense-K is instantiated for M in {4, 8, 16, 32} only (spmm_launch.cuh run_densek_m)
   const bool can_densek = (f.m == 4 || f.m == 8 || f.m == 16 || f.m == 32) && (G % 4 == 0);
   const int strategy = opts ? opts->strategy : VENOM_STRATEGY_AUTO;
@@ -582,14 +585,17 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   }
 
   // gathered strategy
-  // values: 2-D [R rows][2G] 16-bit, box 64 × 128 rows, 128B swizzle (UMMA K-major SW128)
+  // values: 2-D [R rows][2G] 16-bit, box 64 × 128 rows, 128B swizzle (UMMA K-major SW128); for
+  // G % 4 != 0 the padded execution form [R][2·G4] (16-byte row pitch)
   CUtensorMap tv, tb;
+  if (padded && !aligned(opts->values_padded, 16)) return VENOM_ERR_INVALID_ARGUMENT;
   {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * G), static_cast<cuuint64_t>(R)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(4 * G)};
+    const int64_t Gp = padded ? (G + 3) / 4 * 4 : G;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * Gp), static_cast<cuuint64_t>(R)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(4 * Gp)};
     cuuint32_t box[2] = {64, 128};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(values), dims, strides, box, es,
+    if (enc(&tv, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(padded ? opts->values_padded : values), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return VENOM_ERR_CUDA;
@@ -738,9 +744,8 @@ venom_status_t venom_order_metadata(const uint8_t* metadata, int64_t R, int64_t 
   venom_status_t st = validate_format(R, K, f);
   if (st != VENOM_OK) return st;
   const int64_t G = K / f.m;
-  if (G % 4 != 0) return VENOM_ERR_UNSUPPORTED_PATTERN;
   if (R == 0 || K == 0) return VENOM_OK;
-  if (!metadata || !metadata_tc || !aligned(metadata_tc, 16) || !aligned(metadata, 2))
+  if (!metadata || !metadata_tc || !aligned(metadata_tc, 16) || (G % 4 == 0 && !aligned(metadata, 2)))
     return VENOM_ERR_INVALID_ARGUMENT;
   if ((st = check_arch()) != VENOM_OK) return st;
   const int64_t num_ks = (G + 31) / 32;
@@ -749,6 +754,27 @@ venom_status_t venom_order_metadata(const uint8_t* metadata, int64_t R, int64_t 
   venom::vnm_order_metadata_kernel<<<static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0,
                                      static_cast<cudaStream_t>(stream)>>>(
       metadata, R, G, num_ks, total, reinterpret_cast<uint32_t*>(metadata_tc));
+  return launch_status();
+}
+
+int64_t venom_values_padded_bytes(int64_t R, int64_t K, venom_format_t f) {
+  if (validate_format(R, K, f) != VENOM_OK) return -1;
+  const int64_t G = K / f.m;
+  return R * ((G + 3) / 4 * 4) * 4;
+}
+
+venom_status_t venom_pad_values(const void* values, int64_t R, int64_t K, venom_format_t f,
+                                void* values_padded, venom_stream_t stream) {
+  venom_status_t st = validate_format(R, K, f);
+  if (st != VENOM_OK) return st;
+  if (R == 0 || K == 0) return VENOM_OK;
+  if (!values || !values_padded || !aligned(values, 4) || !aligned(values_padded, 16)) return VENOM_ERR_INVALID_ARGUMENT;
+  if ((st = check_arch()) != VENOM_OK) return st;
+  const int64_t G = K / f.m, G4 = (G + 3) / 4 * 4;
+  const int64_t blocks = (R * G4 + 255) / 256;
+  venom::vnm_pad_values_kernel<<<static_cast<unsigned>(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0,
+                                 static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint32_t*>(values), R, G, G4, static_cast<uint32_t*>(values_padded));
   return launch_status();
 }
 

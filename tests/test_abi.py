@@ -81,9 +81,23 @@ def test_metadata_tc_sizes_and_errors(L):
     assert L.venom_metadata_tc_bytes(130, 320, f(13, 2, 10)) == 2 * 1 * 128 * 16
     assert L.venom_metadata_tc_bytes(130, 320, f(7, 2, 10)) == -1  # V does not divide R
     fake = P(0x10000)
-    assert L.venom_order_metadata(fake, 256, 8 * 6, f(64, 2, 8), fake, P(0)) == 4  # G % 4 != 0
+    # any G (a partial last 4-group word is completed with 0x4): G = 6 reaches the device check
+    assert L.venom_order_metadata(fake, 256, 8 * 6, f(64, 2, 8), P(0x10008), P(0)) == 1  # misaligned
     assert L.venom_order_metadata(fake, 256, 500, f(64, 2, 8), fake, P(0)) == 3
     assert L.venom_order_metadata(fake, 256, 512, f(64, 2, 8), P(0x10008), P(0)) == 1  # misaligned
+
+
+def test_values_padded_sizes_and_errors(L):
+    """The K' tail's execution form (venom_pad_values): R·ceil(G/4)·4 groups of 4 bytes."""
+    P = ctypes.c_void_p
+    f = venom._Format
+    assert L.venom_values_padded_bytes(256, 330, f(64, 2, 10)) == 256 * 36 * 4  # G = 33 -> 36
+    assert L.venom_values_padded_bytes(128, 640, f(64, 2, 10)) == 128 * 64 * 4  # G = 64: no padding
+    assert L.venom_values_padded_bytes(130, 320, f(7, 2, 10)) == -1
+    fake = P(0x10000)
+    assert L.venom_pad_values(fake, 256, 330, f(64, 2, 10), P(0x10008), P(0)) == 1  # misaligned out
+    assert L.venom_pad_values(fake, 256, 333, f(64, 2, 10), fake, P(0)) == 3
+    assert L.venom_pad_values(P(0), 0, 330, f(64, 2, 10), fake, P(0)) == 0  # R = 0: nothing to do
 
 
 def test_compress_2to4_argument_errors(L):

@@ -374,6 +374,55 @@ def test_spmm_vs_oracle(R, K, T, V, M, dt, bias, tile_t):
         check_spmm(C, C_ref, dt)
 
 
+K_TAIL_CASES = [
+    # R, K, T, V, M, dt — G = K/M not a multiple of 4 (a K' tail): padded values + metadata_tc
+    (256, 330, 136, 64, 10, F16),     # G = 33
+    (128, 2040, 200, 128, 40, BF16),  # G = 51
+    (384, 148, 64, 128, 4, F16),      # M = 4 (contiguous, CTA pair), G = 37
+    (256, 1000, 128, 32, 20, F16),    # V = 32, G = 50
+    (512, 4050, 264, 256, 90, BF16),  # V = 256 (CTA pair), G = 45
+    (192, 70, 72, 64, 10, F16),       # G = 7: a single partial k-stage
+]
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt", K_TAIL_CASES)
+def test_spmm_k_tail_vs_oracle(R, K, T, V, M, dt):
+    """Any G (PAPER.md:223, 271-272 sweep K freely): order_metadata attaches the padded values
+    (venom_pad_values) with the tensor-core metadata, and the SpMM matches the oracle; without the
+    execution form the pattern is refused."""
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 1300 + R + K + M, True)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = vnm_from(parts, R, K, V, M, dt)
+    with pytest.raises(venom.VenomError) as ei:
+        venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt))
+    assert ei.value.status == 4
+    venom.order_metadata(x)
+    assert x.values_padded is not None
+    vp = to_bits(x.values_padded).reshape(R, -1, 2)
+    G = K // M
+    assert np.array_equal(vp[:, :G], parts[0].reshape(R, G, 2)) and not vp[:, G:].any()
+    pairs = [0, 1] + ([2] if M == 4 or V % 256 == 0 else [])
+    for pair in pairs:
+        C = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), cta_pair=pair)
+        check_spmm(C, C_ref, dt)
+    if M != 4:
+        Ct = venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), transposed_out=True)
+        check_spmm(Ct.t().contiguous(), C_ref, dt)
+
+
+def test_spmm_k_tail_after_recompress():
+    """compress(A, out=x) refreshes both execution-form arrays of x (metadata_tc, values_padded)."""
+    R, K, T, V, M = 128, 330, 64, 64, 10
+    A1 = torch.randn(R, K, device="cuda").half()
+    A2 = torch.randn(R, K, device="cuda").half()
+    x = venom.order_metadata(venom.compress(A1, V=V, M=M))
+    B = torch.randn(K, T, device="cuda").half()
+    venom.compress(A2, V=V, M=M, out=x)
+    C = venom.spmm(x, B)
+    ref = venom.decompress(x).float() @ B.float()
+    assert float((C.float() - ref).norm() / ref.norm()) <= TOL_FRO
+
+
 DENSEK_CASES = [
     # R, K, T, V, M, dt, bias — dense-K only shapes: any V, K not a multiple of 128, M = 4 .. 32
     (128, 224, 64, 16, 8, F16, True),
@@ -415,10 +464,13 @@ def tc_order(meta: np.ndarray, R: int, G: int) -> np.ndarray:
     nks = (G + 31) // 32
     mt_n = (R + 127) // 128
 
-    def half(row, g0):
-        if row >= R or g0 >= G:
-            return 0x4444
-        return int(meta[row, g0 // 2]) | (int(meta[row, g0 // 2 + 1]) << 8)
+    def half(row, g0):  # nibbles of groups g0 .. g0+3; rows >= R and groups >= G: the 0x4 code
+        h = 0
+        for t in range(4):
+            g = g0 + t
+            nib = (int(meta[row, g // 2]) >> (4 * (g & 1))) & 0xF if (row < R and g < G) else 0x4
+            h |= nib << (4 * t)
+        return h
     exp = np.zeros((mt_n, nks, 128, 4), np.uint32)
     for mt in range(mt_n):
         for ks in range(nks):
@@ -431,7 +483,7 @@ def tc_order(meta: np.ndarray, R: int, G: int) -> np.ndarray:
 
 
 @pytest.mark.parametrize("R,K,V,M", [(256, 512, 128, 8), (200, 256, 8, 4), (64, 1280, 64, 40),
-                                     (384, 640, 128, 20)])
+                                     (384, 640, 128, 20), (64, 330, 64, 10), (130, 2040, 13, 40)])
 def test_order_metadata_layout(R, K, V, M):
     """venom_order_metadata against the permutation include/venom.h states."""
     A = synth.gaussian((R, K), 1.0, F16, 31)
