@@ -215,7 +215,10 @@ typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, 
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int main(int argc, char** argv) {
+  // argv[1]: L2 promotion of the gather map (0 none, 1 64B, 2 128B, 3 256B); argv[2] = 1: gather cases only
+  const int promo = argc > 1 ? atoi(argv[1]) : 3;
+  const bool only_gather = argc > 2 && atoi(argv[2]) == 1;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   void* fn = nullptr;
@@ -238,7 +241,8 @@ int main() {
   enc(&tt8, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, B, dims, strides, box8, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   enc(&tg, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, B, dims, strides, box1, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CU_TENSOR_MAP_SWIZZLE_128B, static_cast<CUtensorMapL2promotion>(promo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  printf("gather map L2 promotion %d\n", promo);
   enc(&tt, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, B, dims, strides, box128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   enc(&tt64, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, B, dims, strides, box64, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -286,6 +290,7 @@ int main() {
       const int stage = a_bytes + c.rows * 512;
       if (c.S * stage > 220 * 1024 || c.S > 7 || c.ntw + c.nlw + 1 > 16) continue;
       if (gi == 1 && (c.tile == 8 || c.nlw > 0)) continue;
+      if (only_gather && (c.tile || c.nlw || gi == 1)) continue;
       c.iters = 20;
       const CUtensorMap& tile_map = c.tile == 128 ? tt : c.tile == 64 ? tt64 : c.tile == 32 ? tt32 : tt8;
       feed_kernel<<<grid, 512, 226 * 1024>>>(tg, tile_map, ta, ta64, B, c, d);  // warm-up (L2 fill)

@@ -57,6 +57,25 @@ def main():
             check(venom.spmm(y, B, bias=bias), D, B, bias)
         if M % 4 == 0:
             venom.expand_2to4(x, check=True)
+    # round 2b: the K' tail (G = 33: padded values + metadata_tc), V = 64 tile 64 (M64), the
+    # fused all-gather fan-out (row-major and token-major C through the TMA-store epilogue)
+    A = (torch.randn(128, 330, generator=g, device=dev) * 0.02).half()
+    B = torch.randn(330, 64, generator=g, device=dev).half()
+    x = venom.order_metadata(venom.compress(A, V=64, M=10, check=True))
+    D = venom.decompress(x, check=True)
+    check(venom.spmm(x, B), D, B)
+    check(venom.spmm(x, B, transposed_out=True), D, B, transposed=True)
+    A = (torch.randn(192, 640, generator=g, device=dev) * 0.02).half()
+    B = torch.randn(640, 136, generator=g, device=dev).half()
+    x = venom.order_metadata(venom.compress(A, V=64, M=8, check=True))
+    D = venom.decompress(x, check=True)
+    check(venom.spmm(x, B, tile_t=64), D, B)
+    for ct in (False, True):
+        shape = (136, 192) if ct else (192, 136)
+        peers = [torch.empty(shape, dtype=torch.float16, device=dev) for _ in range(2)]
+        C = venom.spmm(x, B, transposed_out=ct, c_peers=peers)
+        check(C, D, B, transposed=ct)
+        assert all(torch.equal(q, C) for q in peers)
     # compressor routes: streaming kernel (tall blocks), tile kernel (lda not 16-byte pitched)
     A = (torch.randn(512, 1024, generator=g, device=dev) * 0.02).half()
     venom.compress(A, V=256, M=128, check=True)
