@@ -65,6 +65,9 @@ SECONDARY_WORKLOAD = "bert_large_ffn_4096tok_64:2:8"  # BASELINE configs[1]
 # contiguous tile boxes with 160 KB in flight per SM on all 148 SMs, no MMA (153 B/ns per SM;
 # 110 B/ns with the sparse MMA reading the same shared memory; tile::gather4 rows reach 84 B/ns).
 FEED_CEILING_GBPS_PER_SM = 153.0
+# tile::gather4 rows (15 issuing warps, the sparse MMAs consuming the same stages): 81 B/ns per SM
+# (profiles/r02_microbench_feed.txt) — the ceiling of the gathered (M > 4) operand's feed
+GATHER4_CEILING_GBPS_PER_SM = 81.2
 FEED_CEILING_SOURCE = ("tools/microbench_feed.cu: TMA tile boxes, 148 SMs, 160 KB in flight per SM, no MMA "
                        "(profiles/r02_microbench_feed.txt; gather4 rows: 84 B/ns per SM)")
 
@@ -417,8 +420,15 @@ def run_gpu(args, ws, rank, local):
                 feed = {"l2_to_smem_bytes_per_launch": xb, "achieved_GBps": round(ach, 1),
                         "ceiling_GBps": round(ceil, 1), "frac": round(ach / ceil, 4),
                         "ceiling_source": FEED_CEILING_SOURCE, "traffic_source": tr.get("source")}
+                if all(L.w["M"] > 4 and not L.expand for L in layers):
+                    # the gathered operand lands through tile::gather4, whose independently
+                    # measured per-SM rate (with the sparse MMAs consuming) is its own ceiling
+                    gceil = GATHER4_CEILING_GBPS_PER_SM * torch.cuda.get_device_properties(device).multi_processor_count
+                    feed["gather4_ceiling_GBps"] = round(gceil, 1)
+                    feed["frac_of_gather4"] = round(ach / gceil, 4)
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_burst, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_burst, 4), "traffic": traffic,
+                "frac_of_nominal_2250": round(achieved / 2250.0, 4),
                 "peak_source": f"{peak_src} bf16 dense burst (MEASURED_PEAKS.json; fp16 runs at the same rate); "
                                f"useful FLOPs of a 2:4 sparse MMA are half its issued FLOPs, so the "
                                f"useful-FLOP peak equals the dense peak",
