@@ -260,6 +260,9 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(feed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
   // {S, rows, rt, ntw, nlw, with_a, tile, mma, cpa}
   std::vector<Cfg> cases = {
+      // gather4 with and without the 16 KB A box (what multicasting A across a 2-CTA cluster saves)
+      {2, 128, 128, 11, 0, 0, 0, 1, 0}, {2, 128, 128, 15, 0, 0, 0, 1, 0}, {2, 128, 128, 15, 0, 1, 0, 1, 0},
+      {2, 128, 128, 15, 0, 0, 0, 0, 0},
       // cp.async only, and cp.async beside gather4 (round 2b)
       {2, 128, 0, 1, 8, 1, 0, 0, 1}, {2, 128, 0, 1, 14, 1, 0, 0, 1}, {5, 64, 0, 1, 14, 1, 0, 0, 1},
       {3, 96, 0, 1, 14, 1, 0, 0, 1},
