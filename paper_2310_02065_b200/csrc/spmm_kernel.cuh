@@ -94,8 +94,12 @@ struct SpmmCfg {
   // D and metadata addresses both offset by 16b lanes; probed in tools/probe_m64.cu). Both blocks
   // share one BN-column accumulator: no wasted tensor work or TMEM, so the accumulator is
   // double-buffered. V = 32 (NB = 4) keeps one M = 128 MMA per block into its own columns.
-  static constexpr bool M64 = (NB_ == 2);
-  static constexpr int ACC_COLS = (M64 ? 1 : NB) * MB_ * BN;
+  // V = 32 (NB = 4) uses the same lane halves: M = 64 MMAs over rows 0-63 (lane offset 0) and
+  // 64-127 (offset 16), each half run once per V-block of B' with the block's result kept: blocks
+  // 0 / 2 write columns [0, BN), blocks 1 / 3 columns [BN, 2·BN) (half the wasted tensor work and
+  // TMEM of one M = 128 MMA per block, so the accumulator is double-buffered at BN = 64).
+  static constexpr bool M64 = (NB_ == 2 || NB_ == 4);
+  static constexpr int ACC_COLS = (M64 ? NB / 2 : NB) * MB_ * BN;
   // TMEM: accumulators, then 4 metadata columns per row block and stage
   static constexpr int E_PER_STAGE = 4 * MB_;
   static constexpr int ACC_BUFS = (2 * ACC_COLS + E_PER_STAGE * STAGES_ <= 512) ? 2 : 1;
@@ -236,14 +240,18 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
           for (int b = 0; b < NB * Cfg::MB; ++b) {
             // MB = 2: row block b has its own A tile and metadata, the B tile is shared;
             // NB > 1: V-block b has its own gathered B', the A tile is shared
-            // M64: block b's accumulator and metadata sit 16·b lanes into every lane quarter
-            const uint32_t lane_off = Cfg::M64 ? (static_cast<uint32_t>(16 * b) << 16) : 0u;
+            // M64: block b's accumulator and metadata sit 16·h lanes into every lane quarter, h the
+            // 64-row half of the tile holding the block (NB = 2: h = b; NB = 4: h = b / 2, and the
+            // odd block of a half writes the second BN columns)
+            const int half = (NB == 4) ? (b >> 1) : b;
+            const uint32_t lane_off = Cfg::M64 ? (static_cast<uint32_t>(16 * half) << 16) : 0u;
+            const uint32_t col_off = (Cfg::M64 && NB == 4) ? static_cast<uint32_t>((b & 1) * BN) : 0u;
             const uint32_t e_addr = e_tmem + (Cfg::MB > 1 ? 4 * b : 0) + kb + lane_off;
             const uint32_t id2 = e_addr & 1u;  // odd metadata column -> selector id2
             // A: K-major SW128, 8-row groups 1024 B apart; K advance 32 B per K=32 MMA
             // (M64: block b's 64 rows start 8 KB into the tile)
             const uint64_t adesc =
-                smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + (Cfg::M64 ? b * 8192 : 0) + kb * 32,
+                smem_desc(sbase + (Cfg::MB > 1 ? b * Cfg::A_BLOCK : 0) + (Cfg::M64 ? half * 8192 : 0) + kb * 32,
                           16, 1024, 2);
             // B': MN-major SW128, 64-column chunks B_CHUNK apart, 8 K-rows 1024 B apart;
             // K advance 32 rows = 4096 B per MMA
@@ -256,7 +264,7 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
               tc_mma_sp_f16_2sm(d_tile + b * BN, adesc, bdesc, idesc | id2, e_addr & ~1u,
                                 (ks | kb) != 0 ? 1u : 0u);
             else
-              tc_mma_sp_f16(Cfg::M64 ? d_tile + lane_off : d_tile + b * BN, adesc, bdesc, idesc | id2,
+              tc_mma_sp_f16(Cfg::M64 ? d_tile + lane_off + col_off : d_tile + b * BN, adesc, bdesc, idesc | id2,
                             e_addr & ~1u, (ks | kb) != 0 ? 1u : 0u);
           }
         }
@@ -316,7 +324,9 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
     tc_fence_after();
     if (warp == Cfg::W_EPI && lane == 0) VENOM_TRACE_EVENT(9, tl);
     const int64_t row = static_cast<int64_t>(m_tile) * (128 * CG) + r_local;
-    const int b = (NB == 1 || Cfg::M64) ? 0 : (32 * q) / p.V;  // warp-uniform block of this lane quarter
+    // warp-uniform accumulator column block of this lane quarter (M64 with NB = 4: quarters 2, 3
+    // hold the odd blocks, written at columns [BN, 2·BN))
+    const int b = (NB == 1 || (Cfg::M64 && NB == 2)) ? 0 : (Cfg::M64 ? (q >> 1) : (32 * q) / p.V);
     const float bv = (p.bias != nullptr && row < p.R)
                          ? (kBF16 ? __uint_as_float(static_cast<uint32_t>(p.bias[row]) << 16)
                                   : __half2float(__ushort_as_half(p.bias[row])))

@@ -133,7 +133,7 @@ venom_status_t run_gather(int NBg, int pair, int tile_t, const CUtensorMap& tv, 
     if (tile_t == 128) return run_spmm<SpmmCfg<2, 128, 2, PRE ? 11 : 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
     if (tile_t == 64) return run_spmm<SpmmCfg<2, 64, 4, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   } else {
-    if (tile_t == 64) return run_spmm<SpmmCfg<4, 64, 2, 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
+    if (tile_t == 64) return run_spmm<SpmmCfg<4, 64, 2, PRE ? 11 : 8, 1, PRE>, kBF16>(tv, tb, te, tc, p, max_ctas, s);
   }
   return VENOM_ERR_INVALID_ARGUMENT;  // tile override not available for this V
 }

@@ -663,10 +663,10 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     // rows r for V = 64 (each warp holds two 16-row halves; 32-byte swizzle)
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(T)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldc)};
-    cuuint32_t box[2] = {NBg == 2 ? 16u : 32u, 32};
+    cuuint32_t box[2] = {NBg >= 2 ? 16u : 32u, 32};
     cuuint32_t es[2] = {1, 1};
     if (enc(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            NBg == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            NBg >= 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       p.tma_c = 1;
     else
@@ -675,7 +675,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(R)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * ldc)};
     // V = 64 (two M = 64 blocks per tile): a warp's 32 lanes hold two 16-row halves -> 16-row boxes
-    cuuint32_t box[2] = {32, NBg == 2 ? 16u : 32u};
+    cuuint32_t box[2] = {32, NBg >= 2 ? 16u : 32u};
     cuuint32_t es[2] = {1, 1};
     if (enc(&tc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
@@ -695,8 +695,8 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (!aligned(meta_tc, 16)) return VENOM_ERR_INVALID_ARGUMENT;
   CUtensorMap te;
   p.e4d = 0;
-  if (NBg == 2) {
-    // V = 64: the kernel's TMEM lane order for two M = 64 blocks is a permutation of the stored
+  if (NBg >= 2) {
+    // V = 64 / 32: the kernel's TMEM lane order for two M = 64 blocks is a permutation of the stored
     // 16-lane groups (group x + 4y of a block -> 2x + y, spmm_kernel.cuh M64); a 4-D map with
     // swapped strides does it in one TMA op: dims [256 B][y: 2, 1 KB][x: 4, 256 B][blocks, 2 KB]
     const int64_t blocks = ((R + 127) / 128) * p.num_ks;

@@ -342,6 +342,10 @@ SPMM_CASES = [
     (320, 960, 200, 64, 10, F16, True, 0),
     (448, 1120, 128, 64, 10, BF16, False, 64),
     (192, 880, 136, 64, 20, F16, True, 128),
+    # V = 32 on the same lane halves (two M = 64 MMAs per half, odd blocks in the second BN
+    # columns): three of a tile's four blocks (R = 96), bf16, a partial last k-stage
+    (96, 704, 136, 32, 16, BF16, True, 0),
+    (416, 1120, 64, 32, 10, F16, False, 0),
 ]
 
 
@@ -862,6 +866,7 @@ def test_spmm_degenerate_shapes():
 @pytest.mark.parametrize("R,K,T,V,M,dt,bias", [
     (192, 640, 136, 64, 10, F16, True),    # encoder's 64:2:10 (gathered, two V-blocks per tile)
     (320, 960, 200, 64, 10, BF16, False),  # V = 64, 2.5 row tiles, T tail (16-row C^T boxes)
+    (224, 640, 72, 32, 10, F16, True),     # V = 32: seven blocks (the last tile's fourth is padding)
     (384, 1024, 200, 128, 16, BF16, False),
     (512, 1024, 264, 128, 4, F16, True),   # 2:4 (contiguous, CTA pair)
     (130, 256, 64, 13, 8, F16, True),      # dense-K-only V -> rejected for token-major C

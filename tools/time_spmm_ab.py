@@ -12,7 +12,7 @@ def main():
     name, rounds, specs = sys.argv[1], int(sys.argv[2]), sys.argv[3:] or [""]
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    L = bench.Layer(name, dev, 0)
+    L = bench.Layer(name, dev, 0, form=os.environ.get("FORM", "auto"))  # FORM=vnm: the gathered form
     st = torch.cuda.current_stream(dev)
     kws = [{k: int(v) for k, v in (x.split("=") for x in s.split(",") if x)} for s in specs]
     for kw in kws:
