@@ -404,11 +404,12 @@ int32_t venom_prefer_2to4(int64_t R, int64_t K, int64_t T, venom_format_t f) {
   if ((K / 4) % 4 != 0 || T < 256) return 0;
   // the fused preparation (venom_compress_2to4) must apply
   if (f.m % 8 != 0 || 128 % f.m != 0 || f.v % 16 != 0 || f.v > 256 || K % 16 != 0) return 0;
-  // measured crossover (profiles/r01_vscaling_sweep.txt, 4096³ for V in
+  // measured crossover (profiles/r02b_vscaling.txt, 4096³ for V in
   // {32, 64, 128, 256} and M in {8, 16, 32}): the gathered path lands bytes per useful FLOP that
   // fall with V and M, while the V:2:4 form's time does not depend on V or M; the V:2:4 form wins
-  // for M = 8 at every V, and for V·M <= 1024 otherwise
-  return (f.m <= 8 || static_cast<int64_t>(f.v) * f.m <= 1024) ? 1 : 0;
+  // for M = 8 below V = 256 and for V·M < 1024 otherwise (round 2's M64 lane-half MMAs moved the
+  // crossover: 64:2:16 and 256:2:8 now run faster gathered)
+  return ((f.m <= 8 && f.v < 256) || static_cast<int64_t>(f.v) * f.m < 1024) ? 1 : 0;
 }
 
 venom_status_t venom_expand_2to4(const void* values, const uint8_t* metadata,

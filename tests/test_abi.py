@@ -163,9 +163,11 @@ def test_no_cpu_fallback_without_device(L):
     assert st in (8, 9)
 
 
-@pytest.mark.parametrize("V,M,expect", [(32, 8, 1), (256, 8, 1), (64, 16, 1), (128, 16, 0), (256, 16, 0),
-                                        (32, 32, 1), (64, 32, 0), (128, 4, 0), (64, 10, 0)])
+@pytest.mark.parametrize("V,M,expect", [(32, 8, 1), (128, 8, 1), (256, 8, 0), (32, 16, 1), (64, 16, 0),
+                                        (128, 16, 0), (256, 16, 0), (32, 32, 0), (64, 32, 0), (128, 4, 0),
+                                        (64, 10, 0)])
 def test_planner_operand_form(L, V, M, expect):
-    """venom_prefer_2to4 follows the measured V-scaling crossover (DESIGN.md planner table): the
-    V:2:4 form for M = 8 or V·M <= 1024; never for M = 4 (already 2:4) or M % 4 != 0."""
+    """venom_prefer_2to4 follows the measured V-scaling crossover (DESIGN.md planner table,
+    profiles/r02b_vscaling.txt): the V:2:4 form for M = 8 below V = 256 or V·M < 1024; never for
+    M = 4 (already 2:4) or M % 4 != 0."""
     assert L.venom_prefer_2to4(4096, 4096 if M != 10 else 4160, 4096, venom._Format(V, 2, M)) == expect
