@@ -58,6 +58,8 @@ class _Opts(ctypes.Structure):
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
+# spmm(gelu=...): opts.activation (include/venom.h): GELU erf form (True / "erf") or tanh form ("tanh")
+_ACTIVATIONS = {False: 0, None: 0, True: 1, "erf": 1, "tanh": 2}
 
 
 _lib = None
@@ -292,7 +294,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
          out: Optional[torch.Tensor] = None, tile_t: int = 0, stages: int = 0,
          max_ctas: int = 0, strategy: int = STRATEGY_AUTO, cta_pair: int = 0,
          use_metadata_tc: bool = True, transposed_out: bool = False,
-         b_kmajor: bool = False, gelu: bool = False, group_n: int = 0,
+         b_kmajor: bool = False, gelu=False, group_n: int = 0,
          c_peers=None) -> torch.Tensor:
     """C = A_vnm · B (+ bias) on the sparse tensor cores.
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T], or with
@@ -300,7 +302,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     tensor-core-ordered metadata (order_metadata) it is used unless use_metadata_tc is False.
     ``b_kmajor``: B is token-major dtype[T, K] (M = 4 operands); with ``transposed_out`` this is
     ``F.linear(B, decompress(x))`` on PyTorch-layout activations. ``gelu``: GELU after the bias in
-    the epilogue (row-major B and C). ``c_peers``: the fused all-gather — device addresses (or
+    the epilogue (row-major B and C): True / "erf" the erf form, "tanh" the tanh form. ``c_peers``: the fused all-gather — device addresses (or
     tensors) where the epilogue also stores C, same layout and leading dimension (tp.py)."""
     assert B.is_cuda and B.dim() == 2 and B.stride(1) == 1 and B.shape[1 if b_kmajor else 0] == x.K
     assert B.dtype == x.dtype
@@ -319,7 +321,7 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
         addrs = [p if isinstance(p, int) else p.data_ptr() for p in c_peers]
         peers = (ctypes.c_void_p * len(addrs))(*addrs)
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
-                 1 if b_kmajor else 0, 1 if gelu else 0, group_n,
+                 1 if b_kmajor else 0, _ACTIVATIONS[gelu], group_n,
                  ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p)) if peers is not None else None,
                  len(c_peers) if c_peers else 0, vpad)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),

@@ -292,13 +292,27 @@ __device__ __forceinline__ void mma_role(const SpmmParams& p, int my_tiles, uint
 // TMEM -> +bias (fp32) -> RNE to fp16/bf16 packed in registers; the accumulator buffer is released
 // to the MMA warp as soon as it has been read, and the 16-byte global stores overlap the next
 // tile's main loop (a single TMEM accumulator no longer serialises the epilogue).
-// kGELU: GELU (erf form, torch.nn.functional.gelu) after the bias, in fp32 before the rounding —
-// a separate instantiation (a runtime activation branch slowed every SpMM)
-// (A Chebyshev erfc with a MUFU reciprocal and exp measured no faster than erff: the GELU
-// epilogue's cost is its issue share beside the producers, not erff's length.)
+// kACT: the activation after the bias, in fp32 before the rounding — a separate instantiation per
+// activation (a runtime activation branch slowed every SpMM):
+//   1 GELU, erf form (torch.nn.functional.gelu): erff is ~20 FMA-pipe instructions per element,
+//     which makes the epilogue pace the kernel (+23% on the encoder's FFN1; a Chebyshev erfc with
+//     a MUFU reciprocal and exp measured no faster);
+//   2 GELU, tanh form (F.gelu(approximate="tanh"), the original BERT's and GPT-2/3's): one MUFU
+//     tanh.approx (max relative error 2^-11, below the fp16 output's rounding) and 4 FMAs.
 __device__ __forceinline__ float gelu_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_tanh_f(float v) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * fmaf(0.044715f * v, v * v, v)));
+  return 0.5f * v * (1.0f + t);
+}
+template <int kACT>
+__device__ __forceinline__ float act_f(float v) {
+  if constexpr (kACT == 1) return gelu_f(v);
+  else if constexpr (kACT == 2) return gelu_tanh_f(v);
+  else return v;
+}
 
-template <class Cfg, bool kBF16, int CG = 1, bool kCT = false, bool kGELU = false>
+template <class Cfg, bool kBF16, int CG = 1, bool kCT = false, int kACT = 0>
 __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles, uint32_t tmem_base,
                                               uint32_t accf0, uint32_t acce0, int warp, int lane,
                                               uint32_t stage_smem = 0, const CUtensorMap* tm_c = nullptr) {
@@ -346,10 +360,8 @@ __device__ __forceinline__ void epilogue_role(const SpmmParams& p, int my_tiles,
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if constexpr (kGELU)
-          pk[c][j] = pack2<kBF16>(gelu_f(__uint_as_float(v[2 * j]) + bv), gelu_f(__uint_as_float(v[2 * j + 1]) + bv));
-        else
-          pk[c][j] = pack2<kBF16>(__uint_as_float(v[2 * j]) + bv, __uint_as_float(v[2 * j + 1]) + bv);
+        pk[c][j] = pack2<kBF16>(act_f<kACT>(__uint_as_float(v[2 * j]) + bv),
+                                act_f<kACT>(__uint_as_float(v[2 * j + 1]) + bv));
     }
     tc_fence_before();
     __syncwarp();
@@ -722,7 +734,7 @@ __device__ __forceinline__ void producer_contiguous(const SpmmParams& p, const C
   }
 }
 
-template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false, bool kGELU = false>
+template <class Cfg, bool kBF16, bool kContig, bool kCT, bool kBK = false, int kACT = 0>
 __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
     vnm_spmm_kernel(const __grid_constant__ CUtensorMap tm_values,
                     const __grid_constant__ CUtensorMap tm_b,
@@ -933,7 +945,7 @@ __global__ void __launch_bounds__(Cfg::NUM_THREADS, 1)
   } else if (warp >= Cfg::W_EPI && warp < Cfg::W_EPI + Cfg::EPI_WARPS) {
     const uint32_t slot = smem0 + STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES + (warp - Cfg::W_EPI) * Cfg::EPI_STAGE_BYTES;
     if constexpr (Cfg::MB == 2) epilogue_role_mb2<Cfg, kBF16, CG>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot);
-    else epilogue_role<Cfg, kBF16, CG, kCT, kGELU>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot,
+    else epilogue_role<Cfg, kBF16, CG, kCT, kACT>(p, my_tiles, tmem_base, accf0, acce0, warp, lane, slot,
                                                    p.tma_c ? &tm_c : nullptr);
   } else if constexpr (!Cfg::PRE) {
     // ======================= metadata: canonical nibbles -> TMEM (tensor-core layout) ==========

@@ -75,8 +75,10 @@ venom_status_t run_spmm(const CUtensorMap& tv, const CUtensorMap& tb, const CUte
                                 : vnm_spmm_kernel<Cfg, kBF16, false, false>);
   if constexpr (Cfg::MB == 1) {
     // GELU epilogue (row-major C, row-major B; checked by the caller)
-    if (p.act) kern = p.M == 4 ? vnm_spmm_kernel<Cfg, kBF16, true, false, false, true>
-                               : vnm_spmm_kernel<Cfg, kBF16, false, false, false, true>;
+    if (p.act == 1) kern = p.M == 4 ? vnm_spmm_kernel<Cfg, kBF16, true, false, false, 1>
+                                    : vnm_spmm_kernel<Cfg, kBF16, false, false, false, 1>;
+    if (p.act == 2) kern = p.M == 4 ? vnm_spmm_kernel<Cfg, kBF16, true, false, false, 2>
+                                    : vnm_spmm_kernel<Cfg, kBF16, false, false, false, 2>;
   } else {
     if (p.act) return VENOM_ERR_INVALID_ARGUMENT;
   }

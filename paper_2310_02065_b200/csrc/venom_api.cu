@@ -476,7 +476,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
   if (bk && (f.m != 4 || strategy == VENOM_STRATEGY_DENSE_K || (opts && opts->tile_t == 240) || K % 8 != 0))
     return VENOM_ERR_INVALID_ARGUMENT;
   const int act = opts ? opts->activation : 0;
-  if (act != 0 && (act != 1 || ct || bk || strategy == VENOM_STRATEGY_DENSE_K || !can_gather ||
+  if (act != 0 && ((act != 1 && act != 2) || ct || bk || strategy == VENOM_STRATEGY_DENSE_K || !can_gather ||
                    (opts && opts->tile_t == 240)))
     return VENOM_ERR_INVALID_ARGUMENT;
   const bool has_tc = opts && opts->metadata_tc;

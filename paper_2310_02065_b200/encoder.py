@@ -52,7 +52,7 @@ class SparseLinear:
         self.bias = bias
 
     def __call__(self, x_fm: torch.Tensor, out: Optional[torch.Tensor] = None,
-                 token_major: bool = False, gelu: bool = False) -> torch.Tensor:
+                 token_major: bool = False, gelu=False) -> torch.Tensor:
         assert x_fm.shape[0] == self.K, (x_fm.shape, self.K)
         return spmm(self.op, x_fm, bias=self.bias, out=out, transposed_out=token_major, gelu=gelu)
 
@@ -68,6 +68,9 @@ class EncoderConfig:
     V: int = 64
     M: int = 10
     eps: float = 1e-12
+    # GELU form: "tanh" as the original BERT (and GPT-2/3) define it, the hardware tanh in the SpMM
+    # epilogue; "erf" is torch's default form (its erff epilogue costs FFN1 ~25%)
+    gelu: str = "tanh"
 
     @property
     def tokens(self) -> int:
@@ -164,7 +167,7 @@ class SparseEncoder:
         L["o"](self.attn_fm, out=self.o_tm, token_major=True)
         x1 = torch.empty_like(x)
         enc_add_layernorm(x, self.o_tm, L["ln1_w"], L["ln1_b"], cfg.eps, x1, self.x1_fm)
-        L["f1"](self.x1_fm, out=self.hid[:cfg.ffn], gelu=True)   # GELU in the epilogue; FFN2's B
+        L["f1"](self.x1_fm, out=self.hid[:cfg.ffn], gelu=cfg.gelu)  # GELU in the epilogue; FFN2's B
         L["f2"](self.hid, out=self.f2_tm, token_major=True)
         out = torch.empty_like(x)
         enc_add_layernorm(x1, self.f2_tm, L["ln2_w"], L["ln2_b"], cfg.eps, out, self.x_fm)
@@ -186,7 +189,7 @@ def dense_forward(cfg: EncoderConfig, dense: List[dict], x_tm: torch.Tensor) -> 
         w, b = L["o"]
         x = F.layer_norm(x + torch.addmm(b, a, w.t()), (h,), L["ln1_w"], L["ln1_b"], cfg.eps)
         w, b = L["f1"]
-        f = F.gelu(torch.addmm(b, x, w.t()))
+        f = F.gelu(torch.addmm(b, x, w.t()), approximate="tanh" if cfg.gelu == "tanh" else "none")
         w, b = L["f2"]
         x = F.layer_norm(x + torch.addmm(b, f, w.t()), (h,), L["ln2_w"], L["ln2_b"], cfg.eps)
     return x

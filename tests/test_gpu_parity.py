@@ -732,10 +732,12 @@ def test_encoder_linear_layers_vs_oracle(dt):
         xb[lin.in_f:] = 0  # the encoder's zero K-padding rows
         bits_b = lw[bkey].cpu().view(torch.int16).numpy().view(np.uint16)
         ref = oracle.spmm(*parts, lin.out_f, lin.K, F16, cfg.V, cfg.M, xb, bias=bits_b)
-        if gelu:
+        if gelu and cfg.gelu == "tanh":
+            ref = 0.5 * ref * (1.0 + np.tanh(math.sqrt(2.0 / math.pi) * (ref + 0.044715 * ref ** 3)))
+        elif gelu:
             ref = 0.5 * ref * (1.0 + erf(ref / math.sqrt(2.0)))
         out = torch.empty((T, lin.out_f) if tm else (lin.out_f, T), dtype=torch.float16, device="cuda")
-        got = lin(to_dev(xb, F16), out=out, token_major=tm, gelu=gelu)
+        got = lin(to_dev(xb, F16), out=out, token_major=tm, gelu=cfg.gelu if gelu else False)
         check_spmm(got.t().contiguous() if tm else got, ref, F16)
 
 
@@ -977,11 +979,14 @@ def test_spmm_gelu_epilogue(R, K, T, V, M, dt):
     C_lin = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
     erf = np.vectorize(math.erf)
     C_ref = 0.5 * C_lin * (1.0 + erf(C_lin / math.sqrt(2.0)))
+    C_tanh = 0.5 * C_lin * (1.0 + np.tanh(math.sqrt(2.0 / math.pi) * (C_lin + 0.044715 * C_lin ** 3)))
     x = vnm_from(parts, R, K, V, M, dt)
     for pre in (False, True):
         if pre:
             venom.order_metadata(x)
         check_spmm(venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), gelu=True), C_ref, dt)
+        # the tanh form (opts.activation = 2, hardware tanh.approx) against its fp64 definition
+        check_spmm(venom.spmm(x, to_dev(B, dt), bias=to_dev(bv, dt), gelu="tanh"), C_tanh, dt)
     with pytest.raises(venom.VenomError):
         venom.spmm(x, to_dev(B, dt), gelu=True, transposed_out=True)
 

@@ -28,8 +28,9 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--seq", type=int, default=512)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--gelu", choices=["tanh", "erf"], default="tanh")
     args = ap.parse_args()
-    cfg = enc.EncoderConfig(layers=args.layers, batch=args.batch, seq=args.seq)
+    cfg = enc.EncoderConfig(layers=args.layers, batch=args.batch, seq=args.seq, gelu=args.gelu)
     dev = torch.device("cuda")
     torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
     W = enc.init_weights(cfg, dev)
@@ -47,6 +48,7 @@ def main():
                       "batch": cfg.batch, "seq": cfg.seq, "sparse_ms": round(t_s, 3), "dense_ms": round(t_d, 3),
                       "speedup_e2e": round(t_d / t_s, 3), "rel_fro_vs_dense_on_pruned_weights": rel,
                       "sparse_linear_useful_tflops_per_s": round(fl / (t_s / 1e3) / 1e12, 2),
+                      "gelu": cfg.gelu + " form (sparse epilogue and dense F.gelu alike)",
                       "dtype": "f16", "data": "random-init weights, N(0,1) activations (no checkpoints)"}))
 
 

@@ -37,7 +37,7 @@ for rep in range(12):
     step("heads -> attn_fm", lambda: venom.enc_heads_to_fm(a, m.attn_fm))
     step("o spmm (token-major out)", lambda: L["o"](m.attn_fm, out=m.o_tm, token_major=True))
     step("add + layer_norm (+ fm copy)", lambda: venom.enc_add_layernorm(x, m.o_tm, L["ln1_w"], L["ln1_b"], cfg.eps, x1, m.x1_fm))
-    step("f1 spmm (+ GELU epilogue)", lambda: L["f1"](m.x1_fm, out=m.hid[:cfg.ffn], gelu=True))
+    step("f1 spmm (+ GELU epilogue)", lambda: L["f1"](m.x1_fm, out=m.hid[:cfg.ffn], gelu=cfg.gelu))
     step("f2 spmm (token-major out)", lambda: L["f2"](m.hid, out=m.f2_tm, token_major=True))
     step("add + layer_norm 2 (+ fm copy)", lambda: venom.enc_add_layernorm(x1, m.f2_tm, L["ln2_w"], L["ln2_b"], cfg.eps, o2, m.x_fm))
 torch.cuda.synchronize()
