@@ -1020,6 +1020,52 @@ def test_tensor_parallel_allgather_on_gpu():
             dist.destroy_process_group()
 
 
+def test_tensor_parallel_row_split_on_gpu():
+    """tp's row split (V-block-aligned weight shards): each "rank" runs the
+    SpMM on its shard_rows operand; (a) the shards' row blocks stacked equal the unsharded C bit
+    for bit; (b) the fused variant's epilogue fan-out, emulated with one local buffer per rank and
+    each shard storing into every other buffer at its row offset (the addressing of
+    tp.peer_row_slices), fills every buffer with the full C; (c) the one-rank NCCL group runs
+    spmm_tp_rows_allgather end to end."""
+    import socket
+    import torch.distributed as dist
+    from paper_2310_02065_b200 import tp
+    for (R, K, T, V, M, world) in [(512, 512, 136, 128, 16, 2), (384, 640, 200, 64, 10, 3), (256, 330, 64, 64, 10, 2)]:
+        A, B, bv, parts = oracle_problem(R, K, T, V, M, F16, 83 + R, True)
+        x = venom.order_metadata(vnm_from(parts, R, K, V, M, F16))
+        Bd, bd = to_dev(B, F16), to_dev(bv, F16)
+        C_full = venom.spmm(x, Bd, bias=bd)
+        check_spmm(C_full, oracle.spmm(*parts, R, K, F16, V, M, B, bias=bv), F16)
+        bufs = [torch.full((R, T), float("nan"), dtype=torch.float16, device="cuda") for _ in range(world)]
+        blocks = []
+        for rank in range(world):
+            r0, r1 = tp.row_slice(R, V, world, rank)
+            xr = venom.order_metadata(tp.shard_rows(x, r0, r1))
+            blocks.append(venom.spmm(xr, Bd, bias=bd[r0:r1]))
+            peers = [bufs[q][r0:r1] for q in range(world) if q != rank]
+            venom.spmm(xr, Bd, bias=bd[r0:r1], out=bufs[rank][r0:r1], c_peers=peers)
+        torch.cuda.synchronize()
+        assert torch.equal(torch.cat(blocks, 0), C_full), (R, V, M)
+        for q in range(world):
+            assert torch.equal(bufs[q], C_full), (R, V, M, q)
+    created = False
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0)
+        created = True
+    try:
+        r0, r1 = tp.row_slice(R, V, dist.get_world_size(), dist.get_rank())
+        xr = venom.order_metadata(tp.shard_rows(x, r0, r1))
+        C = tp.spmm_tp_rows_allgather(xr, Bd, bias_rows=bd[r0:r1])
+        torch.cuda.synchronize()
+        assert torch.equal(C, C_full)
+    finally:
+        if created:
+            dist.destroy_process_group()
+
+
 def test_spmm_argument_errors_are_synchronous():
     """out-of-range cta_pair, a non-zero stages override and misaligned metadata /
     column_idx views return VENOM_ERR_INVALID_ARGUMENT before anything is launched."""

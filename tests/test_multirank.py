@@ -96,6 +96,26 @@ def _worker(rank: int, ws: int, port: int, q):
         ps = tp.peer_slices(_H, t0, R, 2, rank)
         assert ps == [b + t0 * R * 2 for r, b in enumerate(_H.buffer_ptrs) if r != rank] and len(ps) == ws - 1
 
+        # row split (tp.row_slice / shard_rows / gather_rows): rank r owns whole V-blocks of rows;
+        # its oracle product on its compressed rows, gathered as row-major blocks, equals the
+        # unsharded product bit for bit, and the row slices tile [0, R)
+        r0, r1 = tp.row_slice(R, V, ws, rank)
+        assert (r0, r1) == (rank * (R // ws), (rank + 1) * (R // ws)) and r0 % V == 0
+        vals, meta, cidx = parts
+        G = K // M
+        part_r = (vals.reshape(R, G, 2)[r0:r1], meta[r0:r1], cidx.reshape(R // V, G, 4)[r0 // V:r1 // V])
+        C_rows = oracle.spmm(*part_r, r1 - r0, K, synth.F16, V, M, B)
+        full_rows = tp.gather_rows(torch.from_numpy(C_rows))
+        if rank == 0:
+            assert np.array_equal(full_rows.numpy(), oracle.spmm(*parts, R, K, synth.F16, V, M, B))
+        # and the rank's own compression of its weight shard gives the same arrays (V-block aligned)
+        own = oracle.compress(np.ascontiguousarray(A[r0:r1]), synth.F16, V=V, M=M)
+        assert all(np.array_equal(a.reshape(-1), b.reshape(-1)) for a, b in zip(own, part_r))
+        with pytest.raises(ValueError):
+            tp.row_slice(R, 48, ws, rank)
+        prs = tp.peer_row_slices(_H, r0, T, 2, rank)
+        assert prs == [b + r0 * T * 2 for r, b in enumerate(_H.buffer_ptrs) if r != rank]
+
         # weak scaling draws per-rank activations: the ranks' B differ
         b_r = torch.from_numpy(synth.gaussian((8, 8), 1.0, synth.F16, 1001 + 7919 * rank).astype(np.int32))
         gb = [torch.empty_like(b_r) for _ in range(ws)]
