@@ -320,6 +320,8 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
         # fused all-gather: device addresses (ints or tensors) of the peer output slices
         addrs = [p if isinstance(p, int) else p.data_ptr() for p in c_peers]
         peers = (ctypes.c_void_p * len(addrs))(*addrs)
+    if gelu not in _ACTIVATIONS:
+        raise ValueError(f"gelu must be False, True / 'erf' or 'tanh', not {gelu!r}")
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
                  1 if b_kmajor else 0, _ACTIVATIONS[gelu], group_n,
                  ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p)) if peers is not None else None,
