@@ -231,9 +231,11 @@ typedef struct {
                         rejected with VENOM_ERR_INVALID_ARGUMENT). 0: row-major C (default). */
   int32_t b_kmajor;    /* 1: B is given K-major (token-major activations, the PyTorch [tokens,
                         features] layout): dtype[T][ldb] with ldb >= K, ldb % 8 == 0. M = 4 operands
-                        only (plain 2:4 or the V:2:4 form of venom_compress_2to4), one accumulator per
-                        CTA (tile_t 240 and DENSE_K rejected). With c_transposed this is
-                        Y = X·Wᵀ on [T, K] activations. 0: B row-major dtype[K][ldb] (default). */
+                        (plain 2:4 or the V:2:4 form of venom_compress_2to4) read it natively, one
+                        accumulator per CTA (tile_t 240 and DENSE_K rejected). M > 4 (gathered)
+                        operands need b_scratch: B is first transposed into it (K % 8 == 0). With
+                        c_transposed this is Y = X·Wᵀ on [T, K] activations. 0: B row-major
+                        dtype[K][ldb] (default). */
   int32_t activation;  /* 1: GELU (erf form, x·Φ(x)) applied after the bias in fp32 before the
                         rounding; 2: GELU, tanh form (0.5·x·(1 + tanh(√(2/π)·(x + 0.044715·x³))), the
                         original BERT's and GPT-2/3's; hardware tanh.approx, max relative error 2^-11,
@@ -256,6 +258,8 @@ typedef struct {
                         to a multiple of 4 groups (venom_pad_values). Needed, with metadata_tc, when
                         G = K/M is not a multiple of 4: the values' TMA map needs a 16-byte row
                         pitch (4·G bytes otherwise). Ignored when G % 4 == 0. 16-byte aligned. */
+  void* b_scratch;     /* nullable DEVICE pointer: dtype[K][T] caller-owned scratch (16-byte aligned)
+                        for b_kmajor with an M > 4 operand (the transposed B the gathered path reads). */
 } venom_spmm_opts_t;
 
 venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const uint8_t* column_idx,

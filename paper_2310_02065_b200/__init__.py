@@ -54,7 +54,7 @@ class _Opts(ctypes.Structure):
                 ("metadata_tc", ctypes.c_void_p), ("c_transposed", ctypes.c_int32),
                 ("b_kmajor", ctypes.c_int32), ("activation", ctypes.c_int32), ("group_n", ctypes.c_int32),
                 ("c_peers", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_int32),
-                ("values_padded", ctypes.c_void_p)]
+                ("values_padded", ctypes.c_void_p), ("b_scratch", ctypes.c_void_p)]
 
 
 STRATEGY_AUTO, STRATEGY_GATHER, STRATEGY_DENSE_K = 0, 1, 2
@@ -300,7 +300,8 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
     B: dtype[K, T] (row stride may exceed T); returns / fills C: dtype[R, T], or with
     ``transposed_out`` the token-major C^T: dtype[T, R] (row stride may exceed R). When x carries
     tensor-core-ordered metadata (order_metadata) it is used unless use_metadata_tc is False.
-    ``b_kmajor``: B is token-major dtype[T, K] (M = 4 operands); with ``transposed_out`` this is
+    ``b_kmajor``: B is token-major dtype[T, K] (read natively by M = 4 operands; transposed once into
+    a scratch buffer for M > 4); with ``transposed_out`` this is
     ``F.linear(B, decompress(x))`` on PyTorch-layout activations. ``gelu``: GELU after the bias in
     the epilogue (row-major B and C): True / "erf" the erf form, "tanh" the tanh form. ``c_peers``: the fused all-gather — device addresses (or
     tensors) where the epilogue also stores C, same layout and leading dimension (tp.py)."""
@@ -320,12 +321,16 @@ def spmm(x: VNMTensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None,
         # fused all-gather: device addresses (ints or tensors) of the peer output slices
         addrs = [p if isinstance(p, int) else p.data_ptr() for p in c_peers]
         peers = (ctypes.c_void_p * len(addrs))(*addrs)
+    scratch = None
+    if b_kmajor and x.M != 4:
+        # the gathered operand reads feature-major B: the library transposes B^T into this scratch
+        scratch = torch.empty((x.K, T), dtype=B.dtype, device=B.device)
     if gelu not in _ACTIVATIONS:
         raise ValueError(f"gelu must be False, True / 'erf' or 'tanh', not {gelu!r}")
     opts = _Opts(tile_t, stages, max_ctas, strategy, cta_pair, mtc, 1 if transposed_out else 0,
                  1 if b_kmajor else 0, _ACTIVATIONS[gelu], group_n,
                  ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p)) if peers is not None else None,
-                 len(c_peers) if c_peers else 0, vpad)
+                 len(c_peers) if c_peers else 0, vpad, scratch.data_ptr() if scratch is not None else None)
     st = lib().venom_spmm_ex(ctypes.c_void_p(x.values.data_ptr()),
                              ctypes.c_void_p(x.metadata.data_ptr() if x.metadata.numel() else 0),
                              ctypes.c_void_p(x.column_idx.data_ptr() if x.column_idx.numel() else 0),

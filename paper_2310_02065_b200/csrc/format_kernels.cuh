@@ -1028,6 +1028,41 @@ __global__ void __launch_bounds__(256) vnm_pad_values_kernel(const uint32_t* __r
   }
 }
 
+// Token-major activations -> feature-major B for the gathered operand (venom_spmm_ex with b_kmajor
+// and M > 4): Y[k][t] = X[t][k], X = dtype[T][ldx], Y = dtype[K][T]. 64 × 64 tiles
+// through shared memory (pitch 65 halves: the column reads of the store pass hit 32 distinct banks);
+// 32-bit global accesses, 128 contiguous bytes per warp in both passes.
+__global__ void __launch_bounds__(256) vnm_transpose16_kernel(const uint16_t* __restrict__ X, int64_t T, int64_t K,
+                                                              int64_t ldx, uint16_t* __restrict__ Y) {
+  __shared__ uint16_t tile[64][65];
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int w = threadIdx.x & 31, r = threadIdx.x >> 5;  // word within a 64-element row, row offset
+  for (int i = r; i < 64; i += 8) {
+    const int64_t t = t0 + i, k = k0 + 2 * w;
+    uint16_t a = 0, b = 0;
+    if (t < T) {
+      if (k + 1 < K && ((ldx & 1) == 0)) {
+        const uint32_t v = __ldcs(reinterpret_cast<const uint32_t*>(X + t * ldx + k));
+        a = static_cast<uint16_t>(v & 0xFFFFu);
+        b = static_cast<uint16_t>(v >> 16);
+      } else {
+        if (k < K) a = X[t * ldx + k];
+        if (k + 1 < K) b = X[t * ldx + k + 1];
+      }
+    }
+    tile[i][2 * w] = a;
+    tile[i][2 * w + 1] = b;
+  }
+  __syncthreads();
+  for (int i = r; i < 64; i += 8) {
+    const int64_t k = k0 + i, t = t0 + 2 * w;
+    if (k >= K) continue;
+    const uint32_t v = static_cast<uint32_t>(tile[2 * w][i]) | (static_cast<uint32_t>(tile[2 * w + 1][i]) << 16);
+    if (t + 1 < T) *reinterpret_cast<uint32_t*>(Y + k * T + t) = v;  // T % 8 == 0: aligned
+    else if (t < T) Y[k * T + t] = static_cast<uint16_t>(v & 0xFFFFu);
+  }
+}
+
 // ------------------------------------------------------------------ masked compression
 // venom_compress_masked (include/venom.h; reading #20): the kept set comes from an
 // external V:N:M mask. One thread per (row block, pair of groups) so that every metadata byte has

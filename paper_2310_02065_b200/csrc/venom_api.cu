@@ -473,7 +473,29 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     return VENOM_ERR_INVALID_ARGUMENT;
   if (ct && (strategy == VENOM_STRATEGY_DENSE_K || !can_gather || (opts && opts->tile_t == 240)))
     return VENOM_ERR_INVALID_ARGUMENT;
-  if (bk && (f.m != 4 || strategy == VENOM_STRATEGY_DENSE_K || (opts && opts->tile_t == 240) || K % 8 != 0))
+  if (bk && f.m != 4) {
+    // gathered operand with token-major activations: the selected K-rows of B would be columns
+    // of B^T, which tile::gather4 cannot fetch; B^T is transposed once into the caller's scratch
+    // (feature-major [K][T], 2·|B| of HBM traffic) and the feature-major path runs on it
+    // (cheaper than compacting raw K-major tiles in shared memory)
+    if (!opts->b_scratch || !aligned(opts->b_scratch, 16) || strategy == VENOM_STRATEGY_DENSE_K ||
+        opts->tile_t == 240 || K % 8 != 0 || ldb < K)
+      return VENOM_ERR_INVALID_ARGUMENT;
+    if ((st = check_arch()) != VENOM_OK) return st;
+    if (K > 0) {
+      const dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((T + 63) / 64));
+      if (grid.y > 65535) return VENOM_ERR_INVALID_ARGUMENT;
+      venom::vnm_transpose16_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          static_cast<const uint16_t*>(B), T, K, ldb, static_cast<uint16_t*>(opts->b_scratch));
+      if ((st = launch_status()) != VENOM_OK) return st;
+    }
+    venom_spmm_opts_t o2 = *opts;
+    o2.b_kmajor = 0;
+    o2.b_scratch = nullptr;
+    return venom_spmm_ex(values, metadata, column_idx, R, K, f, opts->b_scratch, T, T, C, ldc, bias, dt, &o2,
+                         stream);
+  }
+  if (bk && (strategy == VENOM_STRATEGY_DENSE_K || (opts && opts->tile_t == 240) || K % 8 != 0))
     return VENOM_ERR_INVALID_ARGUMENT;
   const int act = opts ? opts->activation : 0;
   if (act != 0 && ((act != 1 && act != 2) || ct || bk || strategy == VENOM_STRATEGY_DENSE_K || !can_gather ||

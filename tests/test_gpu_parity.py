@@ -965,8 +965,32 @@ def test_spmm_kmajor_b_on_2to4_form_is_torch_linear():
     ref = torch.nn.functional.linear(X.float(), venom.decompress(x).float())
     assert (Y.float() - ref).norm() / ref.norm() <= 2e-3
     assert torch.equal(Y.t(), venom.spmm(y, X.t().contiguous()))
-    with pytest.raises(venom.VenomError):  # gathered (M != 4) operands take row-major B only
-        venom.spmm(x, X, b_kmajor=True)
+    # the gathered (M = 8) operand itself with the same K-major activations: B^T transposed into
+    # the scratch first, then bitwise the feature-major result
+    venom.order_metadata(x)
+    assert torch.equal(venom.spmm(x, X, b_kmajor=True), venom.spmm(x, X.t().contiguous()))
+
+
+@pytest.mark.parametrize("R,K,T,V,M,dt,ct", [
+    (256, 1040, 264, 64, 10, F16, False),   # the encoder's 64:2:10, ragged T
+    (384, 1024, 200, 128, 16, BF16, True),  # token-major C too: F.linear on [T, K] activations
+    (192, 2080, 72, 32, 40, F16, False),    # V = 32, a wider ldb (a column slice of [T, K + 8])
+])
+def test_spmm_kmajor_b_gathered(R, K, T, V, M, dt, ct):
+    """K-major B for the gathered operand (b_kmajor with M > 4): the token-major activations are
+    transposed into the scratch (vnm_transpose16_kernel) and the feature-major path runs on them —
+    bitwise its result, and against the oracle."""
+    A, B, bv, parts = oracle_problem(R, K, T, V, M, dt, 950 + R + T, True)
+    C_ref = oracle.spmm(*parts, R, K, dt, V, M, B, bias=bv)
+    x = venom.order_metadata(vnm_from(parts, R, K, V, M, dt))
+    Bd, bd = to_dev(B, dt), to_dev(bv, dt)
+    wide = torch.zeros((T, K + 8), dtype=tdt(dt), device="cuda")
+    wide[:, :K] = Bd.t()
+    Bt = wide[:, :K] if V == 32 else Bd.t().contiguous()
+    C = venom.spmm(x, Bd, bias=bd, transposed_out=ct)
+    Ck = venom.spmm(x, Bt, bias=bd, b_kmajor=True, transposed_out=ct)
+    assert torch.equal(Ck, C)
+    check_spmm(Ck.t().contiguous() if ct else Ck, C_ref, dt)
 
 
 @pytest.mark.parametrize("R,K,T,V,M,dt", [(256, 1040, 264, 64, 10, F16), (512, 1024, 256, 128, 4, BF16),
