@@ -1029,37 +1029,34 @@ __global__ void __launch_bounds__(256) vnm_pad_values_kernel(const uint32_t* __r
 }
 
 // Token-major activations -> feature-major B for the gathered operand (venom_spmm_ex with b_kmajor
-// and M > 4): Y[k][t] = X[t][k], X = dtype[T][ldx], Y = dtype[K][T]. 64 × 64 tiles
-// through shared memory (pitch 65 halves: the column reads of the store pass hit 32 distinct banks);
-// 32-bit global accesses, 128 contiguous bytes per warp in both passes.
+// and M > 4): Y[k][t] = X[t][k], X = dtype[T][ldx], Y = dtype[K][T] (the caller
+// guarantees K % 8 == 0, T % 8 == 0, ldx % 8 == 0 and 16-byte aligned X, Y). 64 × 64 tiles through
+// shared memory stored k-major with a 72-element pitch (16-byte aligned rows): 16-byte global
+// loads and stores in both passes.
 __global__ void __launch_bounds__(256) vnm_transpose16_kernel(const uint16_t* __restrict__ X, int64_t T, int64_t K,
                                                               int64_t ldx, uint16_t* __restrict__ Y) {
-  __shared__ uint16_t tile[64][65];
+  constexpr int P = 72;
+  __shared__ __align__(16) uint16_t tile[64 * P];  // [k][t]
   const int64_t t0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
-  const int w = threadIdx.x & 31, r = threadIdx.x >> 5;  // word within a 64-element row, row offset
-  for (int i = r; i < 64; i += 8) {
-    const int64_t t = t0 + i, k = k0 + 2 * w;
-    uint16_t a = 0, b = 0;
-    if (t < T) {
-      if (k + 1 < K && ((ldx & 1) == 0)) {
-        const uint32_t v = __ldcs(reinterpret_cast<const uint32_t*>(X + t * ldx + k));
-        a = static_cast<uint16_t>(v & 0xFFFFu);
-        b = static_cast<uint16_t>(v >> 16);
-      } else {
-        if (k < K) a = X[t * ldx + k];
-        if (k + 1 < K) b = X[t * ldx + k + 1];
-      }
-    }
-    tile[i][2 * w] = a;
-    tile[i][2 * w + 1] = b;
+  const int vec = threadIdx.x & 7, row = threadIdx.x >> 3;  // 8 × 16-byte vectors per 64-element row
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int tl = row + 32 * j;
+    const int64_t t = t0 + tl, k = k0 + 8 * vec;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (t < T && k < K) v = __ldcs(reinterpret_cast<const uint4*>(X + t * ldx + k));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      tile[(8 * vec + e) * P + tl] = static_cast<uint16_t>((w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
   }
   __syncthreads();
-  for (int i = r; i < 64; i += 8) {
-    const int64_t k = k0 + i, t = t0 + 2 * w;
-    if (k >= K) continue;
-    const uint32_t v = static_cast<uint32_t>(tile[2 * w][i]) | (static_cast<uint32_t>(tile[2 * w + 1][i]) << 16);
-    if (t + 1 < T) *reinterpret_cast<uint32_t*>(Y + k * T + t) = v;  // T % 8 == 0: aligned
-    else if (t < T) Y[k * T + t] = static_cast<uint16_t>(v & 0xFFFFu);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int kl = row + 32 * j;
+    const int64_t k = k0 + kl, t = t0 + 8 * vec;
+    if (k < K && t < T)
+      *reinterpret_cast<uint4*>(Y + k * T + t) = *reinterpret_cast<const uint4*>(tile + kl * P + 8 * vec);
   }
 }
 

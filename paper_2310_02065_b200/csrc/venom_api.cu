@@ -479,7 +479,7 @@ venom_status_t venom_spmm_ex(const void* values, const uint8_t* metadata, const 
     // (feature-major [K][T], 2·|B| of HBM traffic) and the feature-major path runs on it
     // (cheaper than compacting raw K-major tiles in shared memory)
     if (!opts->b_scratch || !aligned(opts->b_scratch, 16) || strategy == VENOM_STRATEGY_DENSE_K ||
-        opts->tile_t == 240 || K % 8 != 0 || ldb < K)
+        opts->tile_t == 240 || K % 8 != 0 || ldb < K || !aligned(B, 16))
       return VENOM_ERR_INVALID_ARGUMENT;
     if ((st = check_arch()) != VENOM_OK) return st;
     if (K > 0) {
