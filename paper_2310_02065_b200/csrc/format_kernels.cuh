@@ -757,10 +757,16 @@ __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
     if (t < ntiles) issue(t, 0);
     if (t + gridDim.x < ntiles) issue(t + gridDim.x, 1);
   }
-  for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+  // (row block, column chunk) of tile t, advanced by the grid stride without a division per tile
+  const int64_t drb = static_cast<int64_t>(gridDim.x) / nchunks, dcc = static_cast<int64_t>(gridDim.x) - drb * nchunks;
+  int64_t rb = t / nchunks, cc = t - rb * nchunks;
+  for (int it = 0; t < ntiles; t += gridDim.x, ++it, rb += drb, cc += dcc) {
+    if (cc >= nchunks) {
+      cc -= nchunks;
+      ++rb;
+    }
     const int b = it & 1;
     mbar_wait(smem_u32(&full[b]), (it >> 1) & 1);
-    const int64_t rb = t / nchunks, cc = t - rb * nchunks;
     compress_tile_process<kBF16, kExpand, MC, GPC, (MC && GPC) ? 256 : 0>(
         TileView{reinterpret_cast<const uint16_t*>(smem_raw + b * lay.tile_bytes), 0,
                                                    static_cast<int>(box_stride / 2), true}, smem_raw,
