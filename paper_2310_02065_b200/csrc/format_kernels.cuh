@@ -745,8 +745,7 @@ __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
   }
   __syncthreads();
   const uint64_t pol = policy_evict_first();
-  auto issue = [&](int64_t t, int b) {  // thread 0: tile t -> buffer b
-    const int64_t rb = t / nchunks, cc = t - rb * nchunks;
+  auto issue = [&](int64_t rb, int64_t cc, int b) {  // thread 0: tile (rb, cc) -> buffer b
     mbar_arrive_expect_tx(smem_u32(&full[b]), tile_bytes);
     for (int x = 0; x < nbox; ++x)
       tma_load_2d(smem_u32(smem_raw + b * lay.tile_bytes + x * box_stride), &tm_a, smem_u32(&full[b]),
@@ -754,8 +753,9 @@ __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
   };
   int64_t t = blockIdx.x;
   if (threadIdx.x == 0) {
-    if (t < ntiles) issue(t, 0);
-    if (t + gridDim.x < ntiles) issue(t + gridDim.x, 1);
+    if (t < ntiles) issue(t / nchunks, t % nchunks, 0);
+    const int64_t t1 = t + gridDim.x;
+    if (t1 < ntiles) issue(t1 / nchunks, t1 % nchunks, 1);
   }
   // (row block, column chunk) of tile t, advanced by the grid stride without a division per tile
   const int64_t drb = static_cast<int64_t>(gridDim.x) / nchunks, dcc = static_cast<int64_t>(gridDim.x) - drb * nchunks;
@@ -773,7 +773,14 @@ __global__ void __launch_bounds__(256) vnm_compress_tma_kernel(
                                           R, K, V, M, G, gpc, rb, cc * gpc, values, metadata, column_idx, status,
                                           values2, meta_tc, dbg, 2);
     __syncthreads();  // every thread is done with buffer b (and the scratch) before it is refilled
-    if (threadIdx.x == 0 && t + 2 * static_cast<int64_t>(gridDim.x) < ntiles) issue(t + 2 * static_cast<int64_t>(gridDim.x), b);
+    if (threadIdx.x == 0 && t + 2 * static_cast<int64_t>(gridDim.x) < ntiles) {
+      int64_t rb2 = rb + 2 * drb, cc2 = cc + 2 * dcc;  // tile t + 2·grid, no division
+      while (cc2 >= nchunks) {
+        cc2 -= nchunks;
+        ++rb2;
+      }
+      issue(rb2, cc2, b);
+    }
   }
 }
 
