@@ -405,14 +405,34 @@ __device__ __forceinline__ void compress_tile_process(
     rank_pass(true);
     __syncthreads();
   }
-  // ---- phase 2b: the four selected columns of each group, ascending (reading #7)
-  for (int q = tid; q < ng; q += nthr) {
-    uint32_t word = 0;
-    int n = 0;
-    for (int j = 0; j < M && n < 4; ++j)
-      if (s_rank[q * M + j]) word |= static_cast<uint32_t>(j) << (8 * n++);
-    reinterpret_cast<uint32_t*>(column_idx)[rb * G + g0 + q] = word;
-    s_sel[q] = word;
+  // ---- phase 2b: the four selected columns of each group, ascending (reading #7). For M dividing
+  // 32 a warp ballot of the selection flags gives every group's mask at once and the group's first
+  // lane extracts the 4 set positions (the serial scan by one thread per group kept every other
+  // warp waiting at the barrier below); otherwise one thread scans its group.
+  if (M <= 32 && (32 % M) == 0 && ncols <= nthr) {
+    const bool sel = tid < ncols && s_rank[tid] != 0;
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, sel);
+    if (tid < ncols && (tid % M) == 0) {
+      uint32_t m = (mask >> (tid & 31)) & (M == 32 ? 0xFFFFFFFFu : ((1u << M) - 1u));
+      uint32_t word = 0;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        word |= static_cast<uint32_t>(__ffs(m) - 1) << (8 * n);
+        m &= m - 1;
+      }
+      const int q = tid / M;
+      reinterpret_cast<uint32_t*>(column_idx)[rb * G + g0 + q] = word;
+      s_sel[q] = word;
+    }
+  } else {
+    for (int q = tid; q < ng; q += nthr) {
+      uint32_t word = 0;
+      int n = 0;
+      for (int j = 0; j < M && n < 4; ++j)
+        if (s_rank[q * M + j]) word |= static_cast<uint32_t>(j) << (8 * n++);
+      reinterpret_cast<uint32_t*>(column_idx)[rb * G + g0 + q] = word;
+      s_sel[q] = word;
+    }
   }
   __syncthreads();
 
