@@ -350,10 +350,17 @@ __device__ __forceinline__ void compress_tile_process(
 
   // ---- phase 2a: rank of column j in its group by (score desc, index asc) = its place in the
   // order the format selects by (reading #5); the 4th and 5th scores of each group are kept
+  // the margin test of phase 1b on a group's 4th and 5th fp32 scores (below)
+  const double tol = 2.1 * static_cast<double>(V + NS) * 0x1p-24;
+  auto decided = [&](int q) -> bool {
+    if (M <= 4) return true;
+    const double s4 = s_th[2 * q], s5 = s_th[2 * q + 1];
+    return (s4 - s5) > tol * s4 && s4 < 1e30;  // false for NaN / overflow (inf - inf)
+  };
   auto rank_pass = [&](bool only_flagged) {
     for (int t = tid; t < ncols; t += nthr) {
       const int q = t / M, j = t - q * M;
-      if (only_flagged && s_th[2 * q + 1] >= 0.0) continue;  // exact pass: flagged groups only
+      if (only_flagged && decided(q)) continue;  // exact pass: flagged groups only
       const double* sc = s_score + q * M;
       const double sj = sc[j];
       int rank = 0;
@@ -367,21 +374,12 @@ __device__ __forceinline__ void compress_tile_process(
   };
   rank_pass(false);
   __syncthreads();
-  // ---- phase 1b: the margin test, and exact scores for the groups that fail it
-  const double tol = 2.1 * static_cast<double>(V + NS) * 0x1p-24;
-  for (int q = tid; q < ng; q += nthr) {
-    bool ok = true;
-    if (M > 4) {
-      const double s4 = s_th[2 * q], s5 = s_th[2 * q + 1];
-      ok = (s4 - s5) > tol * s4 && s4 < 1e30;  // false for NaN / overflow (inf - inf)
-    }
-    s_th[2 * q + 1] = ok ? 1.0 : -1.0;  // flag: >= 0 decided, < 0 exact pass
-  }
-  __syncthreads();
+  // ---- phase 1b: the margin test (evaluated by every thread that needs it, from the 4th and 5th
+  // scores — no separate phase and barrier), and exact scores for the groups that fail it
   bool any_exact = false;
   for (int t = tid; t < ncols; t += nthr) {
     const int q = t / M;
-    if (s_th[2 * q + 1] >= 0.0) continue;
+    if (decided(q)) continue;
     any_exact = true;
     if constexpr (!kBF16) {
       // fp16: every |a| is k·2^-24 with an integer k < 2^40 (k = m for subnormals, (1024 + m) <<
